@@ -1,0 +1,860 @@
+/*
+ * dd_oracle.c -- plain, slow, obviously-correct CPU fp64 oracle of entropic
+ * domain decomposition for optimal transport (arXiv 2001.10986).
+ *
+ * TEST INFRASTRUCTURE: only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs load this.  It shares no code with the
+ * CUDA product path.
+ *
+ * Every function follows the paper step by step, in its order and notation:
+ *   Sinkhorn Y-/X-iteration ........ Remark "Sinkhorn algorithm"
+ *   sub-solver semantics ............ Sec. 6.2, P:1402-1411 (warm start from u,
+ *                                     start with a Y-iteration, L1 X-error
+ *                                     stop <= ||mu_J|| Err, end after Y-iter)
+ *   Algorithm 2 (one sweep) ......... P:1337-1374 (lines 8-13)
+ *   BalanceMeasures ................. P:1412-1414 (rule: DESIGN.md reading A8)
+ *   Truncate ........................ P:1386-1389
+ *   partitions A/B .................. P:1566-1569 (reading A11)
+ *   coarse-to-fine refinement ....... eq. FineBasicMarginals
+ *   eps change keeps eps*log u ...... P:1510
+ *   schedule ........................ P:1553-1561 (reading A12)
+ *   primal score ..................... P:1419, Lemma ScalingKL
+ * The cell solver is DENSE: |X_J| x |Y_J| terms per half-iteration, no
+ * separable trick, global coordinates, libm exp/log, max-stabilised LSE.
+ */
+#include "dd_oracle.h"
+
+#include <float.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define MAX_LAYERS 16
+
+typedef struct {
+    int side, s, nb;
+    double* mu;        /* side*side */
+    double* nu;        /* side*side */
+    double* logmu;     /* side*side, -inf where mu == 0 */
+    double* mass_i;    /* nb*nb : ||mu_i|| */
+} layer_t;
+
+struct ddo_ctx {
+    ddo_options opt;
+    double tau;
+    int n_layers, cur;
+    layer_t L[MAX_LAYERS];
+    double eps, eps_final;
+    /* state of the current layer: basic-cell Y-marginals nu_i as dense boxes */
+    int* box;          /* nb*nb*4: y0r, y0c, hr, hc */
+    double** val;      /* nb*nb arrays hr*hc */
+    double* alphaA;    /* side*side */
+    double* alphaB;
+    long long half_index;
+    int last_part;
+    ddo_sweep_stats stats;
+    char err[512];
+};
+
+static void set_err(ddo_ctx* c, const char* fmt, ...) {
+    if (!c) return;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(c->err, sizeof(c->err), fmt, ap);
+    va_end(ap);
+}
+
+/* ---------------------------------------------------------------- sums -- */
+/* Neumaier compensated summation (reading A17). */
+typedef struct { double s, c; } ksum_t;
+static void ks_add(ksum_t* k, double x) {
+    double t = k->s + x;
+    if (fabs(k->s) >= fabs(x)) k->c += (k->s - t) + x;
+    else k->c += (x - t) + k->s;
+    k->s = t;
+}
+static double ks_get(const ksum_t* k) { return k->s + k->c; }
+
+/* ------------------------------------------------------- dense Sinkhorn -- */
+/* Remark Sinkhorn in log domain with absorbed potentials
+ * f = eps log(u mu), g = eps log(v nu):
+ *   Y-iteration: g(y) = eps log b(y) - eps LSE_x[(f(x) - c(x,y))/eps]
+ *   X-iteration: f(x) = eps log a(x) - eps LSE_y[(g(y) - c(x,y))/eps]
+ * Stop test after the X-iteration on the X-marginal of the plan (f_old, g):
+ *   P_X pi(x) = a(x) exp((f_old - f_new)/eps). */
+static double lse_col(int nx, int ny, const double* f, const double* C, int y, double eps) {
+    double m = -INFINITY;
+    for (int x = 0; x < nx; ++x) {
+        double t = f[x] - C[(size_t)x * ny + y];
+        if (t > m) m = t;
+    }
+    if (m == -INFINITY) return -INFINITY;
+    double s = 0.0;
+    for (int x = 0; x < nx; ++x) s += exp((f[x] - C[(size_t)x * ny + y] - m) / eps);
+    return m + eps * log(s);
+}
+static double lse_row(int ny, const double* g, const double* Crow, double eps) {
+    double m = -INFINITY;
+    for (int y = 0; y < ny; ++y) {
+        double t = g[y] - Crow[y];
+        if (t > m) m = t;
+    }
+    if (m == -INFINITY) return -INFINITY;
+    double s = 0.0;
+    for (int y = 0; y < ny; ++y) s += exp((g[y] - Crow[y] - m) / eps);
+    return m + eps * log(s);
+}
+
+int ddo_sinkhorn_dense(int nx, int ny, const double* a, const double* b, const double* C,
+                       double eps, double tol, int max_iter, double* f, double* g,
+                       int* iters, double* err) {
+    double* fn = (double*)malloc(sizeof(double) * (size_t)(nx > 0 ? nx : 1));
+    if (!fn) return DDO_ENOMEM;
+    int it = 0, rc = DDO_ENOCONV;
+    double e = INFINITY;
+    while (1) {
+        /* Y-iteration */
+        for (int y = 0; y < ny; ++y)
+            g[y] = (b[y] > 0.0) ? eps * log(b[y]) - lse_col(nx, ny, f, C, y, eps) : -INFINITY;
+        /* X-iteration */
+        for (int x = 0; x < nx; ++x)
+            fn[x] = (a[x] > 0.0) ? eps * log(a[x]) - lse_row(ny, g, C + (size_t)x * ny, eps)
+                                 : -INFINITY;
+        /* L1 error of the X-marginal of the plan (f, g) */
+        e = 0.0;
+        for (int x = 0; x < nx; ++x)
+            if (a[x] > 0.0) e += a[x] * fabs(expm1((f[x] - fn[x]) / eps));
+        ++it;
+        if (e <= tol) { rc = DDO_OK; break; }
+        if (it >= max_iter) { rc = DDO_ENOCONV; break; }
+        memcpy(f, fn, sizeof(double) * (size_t)nx);
+    }
+    free(fn);
+    if (iters) *iters = it;
+    if (err) *err = e;
+    if (!isfinite(e)) return DDO_ENUMERIC;
+    return rc;
+}
+
+/* -------------------------------------------------------------- schedule -- */
+/* at each layer eps = 2 dx_l^2 for 4 sweeps, then dx_l^2 and
+ * 0.5 dx_l^2 for 2 sweeps each, then refine.  Finest layer: keep halving
+ * (2 sweeps each) down to kappa_final (paper: 0.25; BASELINE: 0.5).
+ * eps_start (config 2): prepend kappa_start, kappa_start/2, ... > 2 at the
+ * coarsest layer, 2 sweeps each (reading A12). */
+int ddo_build_schedule(int n_final, int coarsest_side, double kappa_final, double eps_start,
+                       int* side, double* kappa, int* sweeps, int max) {
+    int k = 0;
+#define PUSH(S, K, W)                                                      \
+    do {                                                                   \
+        if (k < max) { side[k] = (S); kappa[k] = (K); sweeps[k] = (W); }   \
+        ++k;                                                               \
+    } while (0)
+    if (coarsest_side <= 0) coarsest_side = 8;
+    if (coarsest_side > n_final) coarsest_side = n_final;
+    for (int sd = coarsest_side; sd <= n_final; sd *= 2) {
+        int finest = (sd == n_final);
+        if (sd == coarsest_side && eps_start > 0.0) {
+            double ks = eps_start * (double)sd * (double)sd;
+            for (double kk = ks; kk > 2.0 * (1.0 + 1e-12); kk *= 0.5) PUSH(sd, kk, 2);
+        }
+        if (finest && kappa_final > 2.0 * (1.0 + 1e-12)) {
+            PUSH(sd, kappa_final, 4);
+            continue;
+        }
+        PUSH(sd, 2.0, 4);
+        if (!finest) {
+            PUSH(sd, 1.0, 2);
+            PUSH(sd, 0.5, 2);
+        } else {
+            for (double kk = 1.0; kk >= kappa_final * (1.0 - 1e-12); kk *= 0.5) PUSH(sd, kk, 2);
+        }
+    }
+#undef PUSH
+    return k;
+}
+
+/* ------------------------------------------------------------ partitions -- */
+/* A = 2x2 blocks of basic cells; B = same with an offset of one
+ * basic cell (2x1 on edges, 1x1 in corners).  Members in row-major order. */
+static int n_cells_axis(int nb, int part) { return part == 1 ? nb / 2 : nb / 2 + 1; }
+
+static void cell_rows(int nb, int part, int p, int* lo, int* hi) {
+    if (part == 1) { *lo = 2 * p; *hi = 2 * p + 1; }
+    else {
+        *lo = 2 * p - 1 < 0 ? 0 : 2 * p - 1;
+        *hi = 2 * p > nb - 1 ? nb - 1 : 2 * p;
+    }
+}
+
+/* ----------------------------------------------------------------- layers -- */
+static void free_state(ddo_ctx* c) {
+    if (c->val) {
+        int nb = c->L[c->cur].nb;
+        for (int i = 0; i < nb * nb; ++i) free(c->val[i]);
+        free(c->val);
+        c->val = NULL;
+    }
+    free(c->box); c->box = NULL;
+    free(c->alphaA); c->alphaA = NULL;
+    free(c->alphaB); c->alphaB = NULL;
+}
+
+static int alloc_state(ddo_ctx* c) {
+    layer_t* L = &c->L[c->cur];
+    size_t nb2 = (size_t)L->nb * L->nb, n2 = (size_t)L->side * L->side;
+    c->box = (int*)calloc(nb2 * 4, sizeof(int));
+    c->val = (double**)calloc(nb2, sizeof(double*));
+    c->alphaA = (double*)calloc(n2, sizeof(double));
+    c->alphaB = (double*)calloc(n2, sizeof(double));
+    return (c->box && c->val && c->alphaA && c->alphaB) ? DDO_OK : DDO_ENOMEM;
+}
+
+/* Product initialisation nu_i = ||mu_i|| nu (reading A3), alpha = 0. */
+static int product_init(ddo_ctx* c) {
+    layer_t* L = &c->L[c->cur];
+    int nb = L->nb, n = L->side;
+    for (int i = 0; i < nb * nb; ++i) {
+        c->box[4 * i + 0] = 0; c->box[4 * i + 1] = 0;
+        c->box[4 * i + 2] = n; c->box[4 * i + 3] = n;
+        c->val[i] = (double*)malloc(sizeof(double) * (size_t)n * n);
+        if (!c->val[i]) return DDO_ENOMEM;
+        for (int y = 0; y < n * n; ++y) c->val[i][y] = L->mass_i[i] * L->nu[y];
+    }
+    return DDO_OK;
+}
+
+void ddo_free(ddo_ctx* c) {
+    if (!c) return;
+    free_state(c);
+    for (int k = 0; k < c->n_layers; ++k) {
+        free(c->L[k].mu); free(c->L[k].nu); free(c->L[k].logmu); free(c->L[k].mass_i);
+    }
+    free(c);
+}
+
+const char* ddo_last_error(const ddo_ctx* c) { return c ? c->err : "null context"; }
+
+static int is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+
+int ddo_init(ddo_ctx** out, int n, const double* mu, const double* nu, double eps,
+             int cell_size, const ddo_options* opt) {
+    if (!out) return DDO_EINVAL;
+    *out = NULL;
+    ddo_ctx* c = (ddo_ctx*)calloc(1, sizeof(ddo_ctx));
+    if (!c) return DDO_ENOMEM;
+    if (opt) c->opt = *opt;
+    if (c->opt.err_tol <= 0) c->opt.err_tol = 1e-6;
+    if (c->opt.max_inner_iter <= 0) c->opt.max_inner_iter = 10000;
+    c->tau = c->opt.trunc_tau == 0.0 ? 1e-15 : (c->opt.trunc_tau < 0 ? 0.0 : c->opt.trunc_tau);
+    if (c->opt.no_truncate) c->tau = 0.0;
+    *out = c;
+    if (!is_pow2(n) || n < 4) { set_err(c, "n=%d must be a power of two >= 4", n); return DDO_EINVAL; }
+    if (!is_pow2(cell_size) || cell_size > n / 2 || (n / cell_size) % 2) {
+        set_err(c, "cell_size=%d must be a power of two with n/s even", cell_size);
+        return DDO_EINVAL;
+    }
+    if (!(eps > 0.0) || !isfinite(eps)) { set_err(c, "eps must be > 0"); return DDO_EINVAL; }
+    if (!mu || !nu) { set_err(c, "null marginal"); return DDO_EINVAL; }
+    double smu = 0, snu = 0;
+    for (size_t k = 0; k < (size_t)n * n; ++k) {
+        if (!isfinite(mu[k]) || mu[k] < 0 || !isfinite(nu[k]) || nu[k] < 0) {
+            set_err(c, "marginals must be finite and >= 0 (index %zu)", k);
+            return DDO_EINVAL;
+        }
+        smu += mu[k]; snu += nu[k];
+    }
+    if (!(smu > 0) || fabs(smu - snu) > 1e-12 * smu) {
+        set_err(c, "||mu|| = %.17g != ||nu|| = %.17g", smu, snu);
+        return DDO_EINVAL;
+    }
+    int coarsest = n;
+    if (c->opt.schedule == DDO_SCHED_LADDER) {
+        coarsest = c->opt.coarsest_side > 0 ? c->opt.coarsest_side : 8;
+        if (!is_pow2(coarsest) || coarsest < 4) { set_err(c, "bad coarsest_side"); return DDO_EINVAL; }
+        if (coarsest > n) coarsest = n;
+    }
+    /* layers coarsest .. n; images by 2x2 sum pooling of the finest (A20) */
+    int nl = 0;
+    for (int sd = coarsest; sd <= n; sd *= 2) ++nl;
+    if (nl > MAX_LAYERS) { set_err(c, "too many layers"); return DDO_EINVAL; }
+    c->n_layers = nl;
+    for (int k = nl - 1; k >= 0; --k) {
+        layer_t* L = &c->L[k];
+        L->side = coarsest << k;
+        L->s = cell_size < L->side / 2 ? cell_size : L->side / 2;   /* reading A19 */
+        L->nb = L->side / L->s;
+        size_t n2 = (size_t)L->side * L->side;
+        L->mu = (double*)malloc(sizeof(double) * n2);
+        L->nu = (double*)malloc(sizeof(double) * n2);
+        L->logmu = (double*)malloc(sizeof(double) * n2);
+        L->mass_i = (double*)calloc((size_t)L->nb * L->nb, sizeof(double));
+        if (!L->mu || !L->nu || !L->logmu || !L->mass_i) return DDO_ENOMEM;
+        if (k == nl - 1) {
+            memcpy(L->mu, mu, sizeof(double) * n2);
+            memcpy(L->nu, nu, sizeof(double) * n2);
+        } else {
+            layer_t* F = &c->L[k + 1];
+            for (int i = 0; i < L->side; ++i)
+                for (int j = 0; j < L->side; ++j) {
+                    size_t a = (size_t)(2 * i) * F->side + 2 * j;
+                    L->mu[(size_t)i * L->side + j] =
+                        F->mu[a] + F->mu[a + 1] + F->mu[a + F->side] + F->mu[a + F->side + 1];
+                    L->nu[(size_t)i * L->side + j] =
+                        F->nu[a] + F->nu[a + 1] + F->nu[a + F->side] + F->nu[a + F->side + 1];
+                }
+        }
+        for (size_t q = 0; q < n2; ++q) L->logmu[q] = L->mu[q] > 0 ? log(L->mu[q]) : -INFINITY;
+        for (int i = 0; i < L->side; ++i)
+            for (int j = 0; j < L->side; ++j)
+                L->mass_i[(i / L->s) * L->nb + (j / L->s)] += L->mu[(size_t)i * L->side + j];
+        for (int q = 0; q < L->nb * L->nb; ++q)
+            if (!(L->mass_i[q] > 0)) {
+                set_err(c, "basic cell %d of layer side %d has zero mass (P:299)", q, L->side);
+                return DDO_EINVAL;
+            }
+    }
+    c->cur = 0;
+    c->eps_final = eps;
+    c->eps = (c->opt.schedule == DDO_SCHED_LADDER) ? 2.0 / ((double)coarsest * coarsest) : eps;
+    int rc = alloc_state(c);
+    if (rc) { set_err(c, "out of memory"); return rc; }
+    rc = product_init(c);
+    if (rc) { set_err(c, "out of memory"); return rc; }
+    c->half_index = 0;
+    c->last_part = 0;
+    return DDO_OK;
+}
+
+int ddo_set_eps(ddo_ctx* c, double eps) {
+    if (!c || !(eps > 0.0)) return DDO_EINVAL;
+    c->eps = eps;   /* alpha = eps log u is kept constant (reading A13) */
+    return DDO_OK;
+}
+
+/* --------------------------------------------------------- one cell solve -- */
+typedef struct {
+    int members[4], nmem;        /* basic-cell indices */
+    int mr[4], mc[4];            /* member basic row/col */
+    int R0, C0, ar, ac;          /* X pixel region */
+    int yr0, yc0, br, bc;        /* union Y box */
+} cellgeo_t;
+
+static void cell_geometry(const ddo_ctx* c, int part, int cidx, cellgeo_t* G) {
+    const layer_t* L = &c->L[c->cur];
+    int nca = n_cells_axis(L->nb, part);
+    int p = cidx / nca, q = cidx % nca;
+    int rlo, rhi, clo, chi;
+    cell_rows(L->nb, part, p, &rlo, &rhi);
+    cell_rows(L->nb, part, q, &clo, &chi);
+    G->nmem = 0;
+    for (int r = rlo; r <= rhi; ++r)
+        for (int cc = clo; cc <= chi; ++cc) {
+            G->mr[G->nmem] = r; G->mc[G->nmem] = cc;
+            G->members[G->nmem++] = r * L->nb + cc;
+        }
+    G->R0 = rlo * L->s; G->C0 = clo * L->s;
+    G->ar = (rhi - rlo + 1) * L->s; G->ac = (chi - clo + 1) * L->s;
+    /* union bounding box of the member boxes (empty boxes ignored) */
+    int y0 = 1 << 30, x0 = 1 << 30, y1 = -1, x1 = -1;
+    for (int m = 0; m < G->nmem; ++m) {
+        const int* b = &c->box[4 * G->members[m]];
+        if (b[2] <= 0 || b[3] <= 0) continue;
+        if (b[0] < y0) y0 = b[0];
+        if (b[1] < x0) x0 = b[1];
+        if (b[0] + b[2] - 1 > y1) y1 = b[0] + b[2] - 1;
+        if (b[1] + b[3] - 1 > x1) x1 = b[1] + b[3] - 1;
+    }
+    if (y1 < 0) { G->yr0 = G->yc0 = 0; G->br = G->bc = 0; }
+    else { G->yr0 = y0; G->yc0 = x0; G->br = y1 - y0 + 1; G->bc = x1 - x0 + 1; }
+}
+
+/* Dense problem of one composite cell: a = mu_J, b = nu_cell = sum_{i in J} nu_i
+ * (Alg. 2 line 8), cost c(x,y) = |x-y|^2 in [0,1]^2 units, f = alpha + eps log mu. */
+typedef struct {
+    int nx, ny;
+    double *a, *b, *C, *f, *g;
+} cellprob_t;
+
+static void free_prob(cellprob_t* P) {
+    free(P->a); free(P->b); free(P->C); free(P->f); free(P->g);
+    memset(P, 0, sizeof(*P));
+}
+
+static int build_prob(const ddo_ctx* c, const cellgeo_t* G, const double* alpha, cellprob_t* P) {
+    const layer_t* L = &c->L[c->cur];
+    double h = 1.0 / L->side;
+    P->nx = G->ar * G->ac;
+    P->ny = G->br * G->bc;
+    P->a = (double*)malloc(sizeof(double) * (size_t)P->nx);
+    P->f = (double*)malloc(sizeof(double) * (size_t)P->nx);
+    P->b = (double*)calloc((size_t)(P->ny > 0 ? P->ny : 1), sizeof(double));
+    P->g = (double*)malloc(sizeof(double) * (size_t)(P->ny > 0 ? P->ny : 1));
+    P->C = (double*)malloc(sizeof(double) * (size_t)P->nx * (size_t)(P->ny > 0 ? P->ny : 1));
+    if (!P->a || !P->f || !P->b || !P->g || !P->C) return DDO_ENOMEM;
+    for (int xr = 0; xr < G->ar; ++xr)
+        for (int xc = 0; xc < G->ac; ++xc) {
+            size_t gx = (size_t)(G->R0 + xr) * L->side + (G->C0 + xc);
+            int x = xr * G->ac + xc;
+            P->a[x] = L->mu[gx];
+            P->f[x] = (L->mu[gx] > 0) ? alpha[gx] + c->eps * L->logmu[gx] : -INFINITY;
+        }
+    for (int m = 0; m < G->nmem; ++m) {
+        const int* bx = &c->box[4 * G->members[m]];
+        const double* v = c->val[G->members[m]];
+        for (int r = 0; r < bx[2]; ++r)
+            for (int q = 0; q < bx[3]; ++q) {
+                int y = (bx[0] + r - G->yr0) * G->bc + (bx[1] + q - G->yc0);
+                P->b[y] += v[(size_t)r * bx[3] + q];
+            }
+    }
+    for (int x = 0; x < P->nx; ++x) {
+        double x1 = (G->R0 + x / G->ac + 0.5) * h, x2 = (G->C0 + x % G->ac + 0.5) * h;
+        for (int y = 0; y < P->ny; ++y) {
+            double y1 = (G->yr0 + y / G->bc + 0.5) * h, y2 = (G->yc0 + y % G->bc + 0.5) * h;
+            P->C[(size_t)x * P->ny + y] = (x1 - y1) * (x1 - y1) + (x2 - y2) * (x2 - y2);
+        }
+    }
+    return DDO_OK;
+}
+
+static double plan_entry(const cellprob_t* P, int x, int y, double eps) {
+    if (P->f[x] == -INFINITY || P->g[y] == -INFINITY) return 0.0;
+    return exp((P->f[x] + P->g[y] - P->C[(size_t)x * P->ny + y]) / eps);
+}
+
+/* BalanceMeasures (reading A8): proportional transfer from
+ * donors (d_i > 0) to receivers (d_i < 0), amount T = min(sum d_+, sum -d_-),
+ * preserving the pointwise sum and non-negativity, no new support. */
+static void balance(int nmem, int ny, double** nu_i, const double* target) {
+    double norm[4], d[4], Dsum = 0, Psum = 0, dmax = 0;
+    for (int m = 0; m < nmem; ++m) {
+        double s = 0;
+        for (int y = 0; y < ny; ++y) s += nu_i[m][y];
+        norm[m] = s;
+        d[m] = s - target[m];
+        if (fabs(d[m]) > dmax) dmax = fabs(d[m]);
+        if (d[m] > 0) Dsum += d[m];
+        else Psum += -d[m];
+    }
+    if (dmax <= 1e-18 || Dsum <= 0 || Psum <= 0) return;
+    double T = Dsum < Psum ? Dsum : Psum;
+    for (int y = 0; y < ny; ++y) {
+        double r = 0;
+        for (int m = 0; m < nmem; ++m)
+            if (d[m] > 0) {
+                double take = nu_i[m][y] * (d[m] / norm[m]) * (T / Dsum);
+                nu_i[m][y] -= take;
+                r += take;
+            }
+        for (int m = 0; m < nmem; ++m)
+            if (d[m] < 0) nu_i[m][y] += r * (-d[m]) / Psum;
+    }
+}
+
+typedef struct { int iters, flag; double err; } cellres_t;
+
+/* Algorithm 2 lines 8-13 for one composite cell J of partition part. */
+static int solve_cell(ddo_ctx* c, int part, int cidx, cellres_t* res) {
+    layer_t* L = &c->L[c->cur];
+    double* alpha = part == 1 ? c->alphaA : c->alphaB;
+    cellgeo_t G;
+    cell_geometry(c, part, cidx, &G);
+    cellprob_t P;
+    memset(&P, 0, sizeof(P));
+    int rc = build_prob(c, &G, alpha, &P);
+    if (rc) { free_prob(&P); return rc; }
+    double muJ = 0;
+    for (int x = 0; x < P.nx; ++x) muJ += P.a[x];
+    /* line 9: pi_cell, u_{C,J} <- Sinkhorn(mu_J, nu_cell, u_{C,J}) */
+    int it = 0;
+    double err = 0;
+    int src = ddo_sinkhorn_dense(P.nx, P.ny, P.a, P.b, P.C, c->eps, muJ * c->opt.err_tol,
+                                 c->opt.max_inner_iter, P.f, P.g, &it, &err);
+    res->iters = it; res->err = err; res->flag = src;
+    /* line 10: nu_i <- P_Y(pi_cell restricted to X_i x Y) */
+    double* nu_i[4];
+    double target[4];
+    for (int m = 0; m < G.nmem; ++m) {
+        nu_i[m] = (double*)calloc((size_t)(P.ny > 0 ? P.ny : 1), sizeof(double));
+        if (!nu_i[m]) { free_prob(&P); return DDO_ENOMEM; }
+        target[m] = L->mass_i[G.members[m]];
+    }
+    for (int x = 0; x < P.nx; ++x) {
+        int xr = x / G.ac, xc = x % G.ac;
+        int br = (G.R0 + xr) / L->s, bcc = (G.C0 + xc) / L->s;
+        int m = 0;
+        while (m < G.nmem && !(G.mr[m] == br && G.mc[m] == bcc)) ++m;
+        for (int y = 0; y < P.ny; ++y) nu_i[m][y] += plan_entry(&P, x, y, c->eps);
+    }
+    /* line 11: BalanceMeasures */
+    balance(G.nmem, P.ny, nu_i, target);
+    /* line 12: Truncate (entries < tau dropped; tight bounding box kept, reading A9/A10) */
+    for (int m = 0; m < G.nmem; ++m) {
+        int y0 = 1 << 30, x0 = 1 << 30, y1 = -1, x1 = -1;
+        for (int y = 0; y < P.ny; ++y) {
+            if (nu_i[m][y] < c->tau || nu_i[m][y] <= 0.0) { nu_i[m][y] = 0.0; continue; }
+            int r = y / G.bc, q = y % G.bc;
+            if (r < y0) y0 = r;
+            if (r > y1) y1 = r;
+            if (q < x0) x0 = q;
+            if (q > x1) x1 = q;
+        }
+        int i = G.members[m];
+        free(c->val[i]);
+        c->val[i] = NULL;
+        int* bx = &c->box[4 * i];
+        if (y1 < 0) { bx[0] = G.yr0; bx[1] = G.yc0; bx[2] = 0; bx[3] = 0; }
+        else {
+            bx[0] = G.yr0 + y0; bx[1] = G.yc0 + x0; bx[2] = y1 - y0 + 1; bx[3] = x1 - x0 + 1;
+            c->val[i] = (double*)malloc(sizeof(double) * (size_t)bx[2] * bx[3]);
+            if (!c->val[i]) { free_prob(&P); return DDO_ENOMEM; }
+            for (int r = 0; r < bx[2]; ++r)
+                for (int q = 0; q < bx[3]; ++q)
+                    c->val[i][(size_t)r * bx[3] + q] = nu_i[m][(size_t)(y0 + r) * G.bc + (x0 + q)];
+        }
+        free(nu_i[m]);
+    }
+    /* store u_{C,J} as alpha = f - eps log mu (plan's f; reading A4) */
+    for (int xr = 0; xr < G.ar; ++xr)
+        for (int xc = 0; xc < G.ac; ++xc) {
+            size_t gx = (size_t)(G.R0 + xr) * L->side + (G.C0 + xc);
+            double fx = P.f[xr * G.ac + xc];
+            alpha[gx] = (L->mu[gx] > 0 && isfinite(fx)) ? fx - c->eps * L->logmu[gx] : 0.0;
+        }
+    free_prob(&P);
+    return DDO_OK;
+}
+
+static int n_cells(const ddo_ctx* c, int part) {
+    int nca = n_cells_axis(c->L[c->cur].nb, part);
+    return nca * nca;
+}
+
+/* Algorithm 2 lines 6-14: one sweep over the selected partition. */
+static int sweep(ddo_ctx* c) {
+    int part = (c->half_index % 2 == 0) ? 1 : 2;   /* l odd -> A (l = half_index+1) */
+    int nc = n_cells(c, part);
+    cellres_t* res = (cellres_t*)calloc((size_t)nc, sizeof(cellres_t));
+    int* rcs = (int*)calloc((size_t)nc, sizeof(int));
+    if (!res || !rcs) { free(res); free(rcs); return DDO_ENOMEM; }
+#ifdef _OPENMP
+    int nt = c->opt.n_threads > 0 ? c->opt.n_threads : omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nt)
+#endif
+    for (int j = 0; j < nc; ++j) rcs[j] = solve_cell(c, part, j, &res[j]);
+    int rc = DDO_OK;
+    ddo_sweep_stats st;
+    memset(&st, 0, sizeof(st));
+    st.cells = nc;
+    for (int j = 0; j < nc; ++j) {     /* fixed-order reduction */
+        if (rcs[j] == DDO_ENOMEM) rc = DDO_ENOMEM;
+        st.iters_sum += res[j].iters;
+        if (res[j].iters > st.iters_max) st.iters_max = res[j].iters;
+        st.err_x_sum += res[j].err;
+        if (res[j].flag != DDO_OK) {
+            st.failed++;
+            if (rc == DDO_OK) rc = res[j].flag;
+        }
+    }
+    layer_t* L = &c->L[c->cur];
+    for (int i = 0; i < L->nb * L->nb; ++i) st.entries += (long long)c->box[4 * i + 2] * c->box[4 * i + 3];
+    c->stats = st;
+    c->half_index++;
+    c->last_part = part;
+    free(res);
+    free(rcs);
+    if (rc == DDO_ENOCONV) set_err(c, "%d cells hit max_inner_iter", st.failed);
+    if (rc == DDO_ENUMERIC) set_err(c, "non-finite marginal error in %d cells", st.failed);
+    return rc;
+}
+
+int ddo_iterate(ddo_ctx* c, int n_half_iters) {
+    if (!c) return DDO_EINVAL;
+    int rc = DDO_OK;
+    for (int k = 0; k < n_half_iters; ++k) {
+        int r = sweep(c);
+        if (r == DDO_ENOMEM || r == DDO_ENUMERIC) return r;
+        if (r) rc = r;
+    }
+    return rc;
+}
+
+/* ------------------------------------------------------------ refinement -- */
+/* eq. FineBasicMarginals:
+ *   nu_i^0(y) = nu(y) * nuhat_{Pa(i)}(pa(y)) / nuhat(pa(y)) * mu(X_i) / muhat(Xhat_{Pa(i)})
+ * with 0/0 := 0.  Fine box = 2x the parent box.  alpha cold start (A14). */
+int ddo_refine(ddo_ctx* c) {
+    if (!c) return DDO_EINVAL;
+    if (c->cur + 1 >= c->n_layers) { set_err(c, "already at the finest layer"); return DDO_EINVAL; }
+    layer_t* Lc = &c->L[c->cur];
+    layer_t* Lf = &c->L[c->cur + 1];
+    int nbc = Lc->nb, nbf = Lf->nb;
+    int* nbox = (int*)calloc((size_t)nbf * nbf * 4, sizeof(int));
+    double** nval = (double**)calloc((size_t)nbf * nbf, sizeof(double*));
+    if (!nbox || !nval) return DDO_ENOMEM;
+    for (int ir = 0; ir < nbf; ++ir)
+        for (int ic = 0; ic < nbf; ++ic) {
+            int i = ir * nbf + ic;
+            int jr = ir * nbc / nbf, jc = ic * nbc / nbf;   /* Pa(i) */
+            int j = jr * nbc + jc;
+            const int* pb = &c->box[4 * j];
+            int* fb = &nbox[4 * i];
+            fb[0] = 2 * pb[0]; fb[1] = 2 * pb[1]; fb[2] = 2 * pb[2]; fb[3] = 2 * pb[3];
+            double ratio_mu = Lf->mass_i[i] / Lc->mass_i[j];
+            size_t area = (size_t)fb[2] * fb[3];
+            nval[i] = (double*)malloc(sizeof(double) * (area > 0 ? area : 1));
+            if (!nval[i]) return DDO_ENOMEM;
+            for (int r = 0; r < fb[2]; ++r)
+                for (int q = 0; q < fb[3]; ++q) {
+                    int y1 = fb[0] + r, y2 = fb[1] + q;          /* fine Y pixel */
+                    int p1 = y1 / 2, p2 = y2 / 2;                /* pa(y) */
+                    double nuhat_j = c->val[j][(size_t)(p1 - pb[0]) * pb[3] + (p2 - pb[1])];
+                    double nuhat = Lc->nu[(size_t)p1 * Lc->side + p2];
+                    double nuy = Lf->nu[(size_t)y1 * Lf->side + y2];
+                    nval[i][(size_t)r * fb[3] + q] =
+                        (nuhat > 0.0) ? nuy * (nuhat_j / nuhat) * ratio_mu : 0.0;
+                }
+        }
+    free_state(c);
+    c->cur += 1;
+    c->box = nbox;
+    c->val = nval;
+    size_t n2 = (size_t)Lf->side * Lf->side;
+    c->alphaA = (double*)calloc(n2, sizeof(double));
+    c->alphaB = (double*)calloc(n2, sizeof(double));
+    if (!c->alphaA || !c->alphaB) return DDO_ENOMEM;
+    c->last_part = 0;
+    return DDO_OK;
+}
+
+int ddo_run_schedule(ddo_ctx* c) {
+    if (!c) return DDO_EINVAL;
+    int sides[256], sweeps[256];
+    double kap[256];
+    int ns;
+    if (c->opt.schedule == DDO_SCHED_LADDER) {
+        int nf = c->L[c->n_layers - 1].side;
+        double kf = c->eps_final * (double)nf * nf;
+        ns = ddo_build_schedule(nf, c->L[0].side, kf, c->opt.eps_start, sides, kap, sweeps, 256);
+    } else {
+        ns = 0;
+        set_err(c, "run_schedule needs DDO_SCHED_LADDER");
+        return DDO_EINVAL;
+    }
+    int rc = DDO_OK;
+    for (int k = 0; k < ns && k < 256; ++k) {
+        while (c->L[c->cur].side < sides[k]) {
+            int r = ddo_refine(c);
+            if (r) return r;
+        }
+        double h = 1.0 / sides[k];
+        ddo_set_eps(c, kap[k] * h * h);
+        int r = ddo_iterate(c, sweeps[k]);
+        if (r == DDO_ENOMEM || r == DDO_ENUMERIC) return r;
+        if (r) rc = r;
+    }
+    return rc;
+}
+
+/* ------------------------------------------------------------ evaluation -- */
+/* Primal evaluation (reading A15): for each cell J of the last swept
+ * partition (A if none), rebuild nu_cell = sum_{i in J} nu_i and the cell
+ * plan pi_J = exp((f + g - c)/eps) with f = alpha_{C,J} + eps log mu and g
+ * from one Y-iteration; pi = sum_J pi_J. */
+typedef struct { double cost, ent, l1x, mass; } evalres_t;
+
+static int eval_cell(ddo_ctx* c, int part, int cidx, evalres_t* er, long long* count,
+                     int* xi, int* yi, double* mass, long long base) {
+    layer_t* L = &c->L[c->cur];
+    double* alpha = part == 1 ? c->alphaA : c->alphaB;
+    cellgeo_t G;
+    cell_geometry(c, part, cidx, &G);
+    cellprob_t P;
+    memset(&P, 0, sizeof(P));
+    int rc = build_prob(c, &G, alpha, &P);
+    if (rc) { free_prob(&P); return rc; }
+    for (int y = 0; y < P.ny; ++y)
+        P.g[y] = (P.b[y] > 0.0) ? c->eps * log(P.b[y]) - lse_col(P.nx, P.ny, P.f, P.C, y, c->eps)
+                                : -INFINITY;
+    ksum_t cost = {0, 0}, ent = {0, 0}, l1x = {0, 0}, ms = {0, 0};
+    long long k = 0;
+    for (int x = 0; x < P.nx; ++x) {
+        size_t gx = (size_t)(G.R0 + x / G.ac) * L->side + (G.C0 + x % G.ac);
+        double px = 0;
+        for (int y = 0; y < P.ny; ++y) {
+            double p = plan_entry(&P, x, y, c->eps);
+            if (!(p > 0.0)) continue;
+            size_t gy = (size_t)(G.yr0 + y / G.bc) * L->side + (G.yc0 + y % G.bc);
+            double cxy = P.C[(size_t)x * P.ny + y];
+            /* log(pi/K) = (f+g-c)/eps - log mu(x) - log nu(y) + c/eps, K = exp(-c/eps) mu nu */
+            double logK = -cxy / c->eps + L->logmu[gx] + log(L->nu[gy]);
+            ks_add(&cost, cxy * p);
+            ks_add(&ent, c->eps * p * (log(p) - logK - 1.0));
+            ks_add(&ms, p);
+            px += p;
+            if (xi) {
+                xi[base + k] = (int)gx;
+                yi[base + k] = (int)gy;
+                mass[base + k] = p;
+            }
+            ++k;
+        }
+        ks_add(&l1x, fabs(px - L->mu[gx]));
+    }
+    if (er) { er->cost = ks_get(&cost); er->ent = ks_get(&ent); er->l1x = ks_get(&l1x); er->mass = ks_get(&ms); }
+    if (count) *count = k;
+    free_prob(&P);
+    return DDO_OK;
+}
+
+static int evaluate(ddo_ctx* c, double* cost, double* ent, double* l1x) {
+    int part = c->last_part ? c->last_part : 1;
+    int nc = n_cells(c, part);
+    evalres_t* er = (evalres_t*)calloc((size_t)nc, sizeof(evalres_t));
+    int* rcs = (int*)calloc((size_t)nc, sizeof(int));
+    if (!er || !rcs) { free(er); free(rcs); return DDO_ENOMEM; }
+#ifdef _OPENMP
+    int nt = c->opt.n_threads > 0 ? c->opt.n_threads : omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nt)
+#endif
+    for (int j = 0; j < nc; ++j) rcs[j] = eval_cell(c, part, j, &er[j], NULL, NULL, NULL, NULL, 0);
+    ksum_t a = {0, 0}, b = {0, 0}, d = {0, 0};
+    int rc = DDO_OK;
+    for (int j = 0; j < nc; ++j) {
+        if (rcs[j]) rc = rcs[j];
+        ks_add(&a, er[j].cost); ks_add(&b, er[j].ent); ks_add(&d, er[j].l1x);
+    }
+    if (cost) *cost = ks_get(&a);
+    if (ent) *ent = ks_get(&b);
+    if (l1x) *l1x = ks_get(&d);
+    free(er);
+    free(rcs);
+    return rc;
+}
+
+int ddo_primal_cost(ddo_ctx* c, double* transport_cost, double* entropic) {
+    if (!c) return DDO_EINVAL;
+    return evaluate(c, transport_cost, entropic, NULL);
+}
+
+int ddo_marginal_error(ddo_ctx* c, double* l1_x, double* l1_y) {
+    if (!c) return DDO_EINVAL;
+    int rc = evaluate(c, NULL, NULL, l1_x);
+    if (rc) return rc;
+    /* Y side: sum_i nu_i(y) vs nu(y) (reading A18) */
+    layer_t* L = &c->L[c->cur];
+    size_t n2 = (size_t)L->side * L->side;
+    double* acc = (double*)calloc(n2, sizeof(double));
+    if (!acc) return DDO_ENOMEM;
+    for (int i = 0; i < L->nb * L->nb; ++i) {
+        const int* b = &c->box[4 * i];
+        for (int r = 0; r < b[2]; ++r)
+            for (int q = 0; q < b[3]; ++q)
+                acc[(size_t)(b[0] + r) * L->side + (b[1] + q)] += c->val[i][(size_t)r * b[3] + q];
+    }
+    ksum_t s = {0, 0};
+    for (size_t y = 0; y < n2; ++y) ks_add(&s, fabs(acc[y] - L->nu[y]));
+    free(acc);
+    if (l1_y) *l1_y = ks_get(&s);
+    return DDO_OK;
+}
+
+int ddo_fetch_plan_coo(ddo_ctx* c, long long* count, int* xi, int* yi, double* mass) {
+    if (!c || !count) return DDO_EINVAL;
+    int part = c->last_part ? c->last_part : 1;
+    int nc = n_cells(c, part);
+    long long total = 0;
+    for (int j = 0; j < nc; ++j) {
+        long long k = 0;
+        int rc = eval_cell(c, part, j, NULL, &k, xi ? xi : NULL, yi, mass, total);
+        if (rc) return rc;
+        total += k;
+    }
+    *count = total;
+    return DDO_OK;
+}
+
+int ddo_get_stats(ddo_ctx* c, ddo_sweep_stats* st) {
+    if (!c || !st) return DDO_EINVAL;
+    *st = c->stats;
+    return DDO_OK;
+}
+
+int ddo_get_state_info(ddo_ctx* c, ddo_state_info* info) {
+    if (!c || !info) return DDO_EINVAL;
+    layer_t* L = &c->L[c->cur];
+    info->side = L->side; info->s = L->s; info->nb = L->nb;
+    info->last_partition = c->last_part;
+    info->half_index = c->half_index;
+    info->eps = c->eps;
+    long long e = 0;
+    for (int i = 0; i < L->nb * L->nb; ++i) e += (long long)c->box[4 * i + 2] * c->box[4 * i + 3];
+    info->entries = e;
+    return DDO_OK;
+}
+
+int ddo_get_state(ddo_ctx* c, int* boxes, long long* offsets, double* values,
+                  double* alpha_A, double* alpha_B) {
+    if (!c) return DDO_EINVAL;
+    layer_t* L = &c->L[c->cur];
+    long long off = 0;
+    for (int i = 0; i < L->nb * L->nb; ++i) {
+        const int* b = &c->box[4 * i];
+        if (boxes) memcpy(&boxes[4 * i], b, 4 * sizeof(int));
+        if (offsets) offsets[i] = off;
+        size_t area = (size_t)b[2] * b[3];
+        if (values && area) memcpy(values + off, c->val[i], sizeof(double) * area);
+        off += (long long)area;
+    }
+    size_t n2 = (size_t)L->side * L->side;
+    if (alpha_A) memcpy(alpha_A, c->alphaA, sizeof(double) * n2);
+    if (alpha_B) memcpy(alpha_B, c->alphaB, sizeof(double) * n2);
+    return DDO_OK;
+}
+
+int ddo_set_state(ddo_ctx* c, int side, long long half_index, int last_partition,
+                  const int* boxes, const long long* offsets, const double* values,
+                  const double* alpha_A, const double* alpha_B) {
+    if (!c || !boxes || !offsets || !values) return DDO_EINVAL;
+    int k = 0;
+    while (k < c->n_layers && c->L[k].side != side) ++k;
+    if (k == c->n_layers) { set_err(c, "no layer of side %d", side); return DDO_EINVAL; }
+    free_state(c);
+    c->cur = k;
+    int rc = alloc_state(c);
+    if (rc) return rc;
+    layer_t* L = &c->L[k];
+    for (int i = 0; i < L->nb * L->nb; ++i) {
+        memcpy(&c->box[4 * i], &boxes[4 * i], 4 * sizeof(int));
+        const int* b = &boxes[4 * i];
+        if (b[2] < 0 || b[3] < 0 || b[0] < 0 || b[1] < 0 || b[0] + b[2] > side || b[1] + b[3] > side) {
+            set_err(c, "box %d out of range", i);
+            return DDO_EINVAL;
+        }
+        size_t area = (size_t)b[2] * b[3];
+        c->val[i] = (double*)malloc(sizeof(double) * (area ? area : 1));
+        if (!c->val[i]) return DDO_ENOMEM;
+        if (area) memcpy(c->val[i], values + offsets[i], sizeof(double) * area);
+    }
+    size_t n2 = (size_t)side * side;
+    if (alpha_A) memcpy(c->alphaA, alpha_A, sizeof(double) * n2);
+    if (alpha_B) memcpy(c->alphaB, alpha_B, sizeof(double) * n2);
+    c->half_index = half_index;
+    c->last_part = last_partition;
+    return DDO_OK;
+}
+
+int ddo_get_layer_marginals(ddo_ctx* c, double* mu, double* nu) {
+    if (!c) return DDO_EINVAL;
+    layer_t* L = &c->L[c->cur];
+    size_t n2 = (size_t)L->side * L->side;
+    if (mu) memcpy(mu, L->mu, sizeof(double) * n2);
+    if (nu) memcpy(nu, L->nu, sizeof(double) * n2);
+    return DDO_OK;
+}

@@ -1,0 +1,186 @@
+/*
+ * dd.h -- C-ABI of the B200 (sm_100a) entropic domain decomposition library
+ *         libdd_gpu.so  (arXiv 2001.10986).
+ *
+ * The hot path is Algorithm 2 of the paper: per
+ * half-iteration ("sweep") every composite cell J of partition A (then B) is
+ * solved as an independent entropic OT problem by log-domain Sinkhorn with
+ * the cell's fixed X-mass mu_J and Y-marginal nu_cell = sum_{i in J} nu_i
+ * (line 8), split back into basic-cell marginals (line 10), balanced
+ * (line 11) and truncated (line 12).  A coarse-to-fine /
+ * eps-scaling driver runs on top.
+ *
+ * Conventions (apply to every entry point):
+ *  - Grid: N x N pixels on [0,1]^2, h = 1/N, pixel centres ((i+1/2)h,(j+1/2)h),
+ *    arrays row-major [i*N + j], i = row (x1), j = column (x2).  X and Y use
+ *    the same grid.  Cost c(x,y) = |x-y|^2.  eps in the same units;
+ *    kappa = eps/h^2 is eps in squared pixels.
+ *  - Potentials: alpha = eps*log u in cost units; the plan of a cell
+ *    is pi(x,y) = exp((alpha(x) + beta(y) - c(x,y))/eps) mu(x) nu(y)
+ *    (K = exp(-c/eps) mu (x) nu).
+ *  - Return codes: DD_OK (0) or one of DD_E*.  No exceptions cross the ABI;
+ *    the message of the last failure is dd_last_error(ctx).
+ *  - Memory: inputs are copied at dd_init (the caller keeps ownership).
+ *    Outputs go to caller buffers; variable-size outputs use the two-call
+ *    pattern (buf == NULL -> required size).  The context owns every device
+ *    allocation and frees it in dd_free.
+ *  - Streams: all device work of a context is issued on one CUDA stream
+ *    (dd_options.stream, or a stream the library creates).  Every entry
+ *    point that returns host data synchronises that stream.
+ *  - Threading: one context per host thread; calls on a context are not
+ *    thread-safe.  One device per context (dd_options.device).
+ *  - Determinism: per-cell arithmetic does not depend on scheduling; all
+ *    reductions are fixed-order.  Results are bit-reproducible run to run.
+ *  - There is NO CPU fallback: without a usable sm_100 device dd_init
+ *    returns DD_ECUDA.
+ */
+#ifndef DD_H
+#define DD_H
+#include <stddef.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DD_OK 0
+#define DD_EINVAL 1    /* invalid argument (n not 2^k, n/s odd, bad mass, ...) */
+#define DD_ENOCONV 2   /* some cell hit max_inner_iter; state stays Y-feasible */
+#define DD_ENUMERIC 3  /* non-finite value in a cell solve */
+#define DD_ECUDA 4     /* CUDA runtime error / no sm_100 device */
+#define DD_ENCCL 5     /* reserved: multi-GPU communication error */
+#define DD_ENOMEM 6    /* device allocation failed or pool capacity exceeded */
+
+#define DD_COST_SQEUCLID 0
+
+#define DD_SCHED_FIXED 0   /* single layer (the input grid), eps fixed by the caller */
+#define DD_SCHED_LADDER 1  /* multiscale + eps-scaling (A12) */
+
+#define DD_FLAG_DEVICE_INPUT 1u  /* dd_init: mu, nu are device pointers (fp64) */
+
+#define DD_PLAN_BASIC_MARGINALS 0
+#define DD_PLAN_COO 1
+
+typedef struct dd_ctx dd_ctx;
+
+typedef struct {                /* zero-initialised fields take the defaults */
+    double err_tol;             /* Err: cell stop when L1 X-error <= ||mu_J|| Err; 0 -> 1e-6 */
+    double trunc_tau;           /* truncation threshold; 0 -> 1e-15, <0 -> 0 */
+    int max_inner_iter;         /* Sinkhorn iterations per cell solve; 0 -> 10000 */
+    int check_every;            /* stop-test cadence; 0/1 -> every iteration (parity mode, A5) */
+    int n_gpus;                 /* reserved for striping; 0/1 -> one GPU */
+    int schedule;               /* DD_SCHED_FIXED | DD_SCHED_LADDER */
+    double eps_start;           /* ladder: eps at the coarsest layer if > 2 h_0^2 (0 = none) */
+    int coarsest_side;          /* ladder: coarsest layer side (0 -> 8) */
+    int no_truncate;            /* 1 -> tau = 0 */
+    unsigned int flags;         /* DD_FLAG_* */
+    int device;                 /* CUDA device ordinal */
+    long long pool_capacity;    /* nu_i pool entries per buffer; 0 -> 48 * N^2 + 2^20 */
+    void* stream;               /* cudaStream_t to use, or NULL */
+    int reserved[8];
+} dd_options;
+
+typedef struct {                /* one sweep (or accumulated totals) */
+    long long cells;            /* composite-cell solves */
+    long long iters_sum;        /* Sinkhorn iterations summed over cells */
+    int iters_max;
+    int failed;                 /* cells that hit max_inner_iter or went non-finite */
+    double err_x_sum;           /* sum_J L1 X-error of the returned plans (<= Err) */
+    long long entries;          /* stored nu_i entries after the sweep */
+    double ms;                  /* device time of the sweep(s), CUDA events */
+    double mufu_ops;            /* MUFU (ex2/lg2/rcp) operations executed by the cell solve */
+    double solve_ms;            /* device time of the cell-solve kernel launches only */
+    long long launches;         /* kernel launches issued */
+    long long big_cells;        /* cells routed to the large-box path */
+    int max_box;                /* largest composite Y-box side seen */
+    int reserved_i;
+} dd_sweep_stats;
+
+typedef struct {
+    int side;                   /* N_l of the current layer */
+    int s;                      /* basic cell side s_l */
+    int nb;                     /* basic cells per axis */
+    int last_partition;         /* 0 none, 1 A, 2 B */
+    long long half_index;       /* sweeps done so far */
+    long long entries;          /* stored nu_i entries */
+    double eps;                 /* current eps ([0,1]^2 units) */
+} dd_state_info;
+
+/* dd_init -- create a context.
+ *  n: grid side (power of two >= 4); mu, nu: n*n fp64 row-major, >= 0,
+ *  finite, ||mu|| = ||nu|| (1e-12 rel.), every basic cell of every layer with
+ *  ||mu_i|| > 0.  Host pointers unless opt->flags has
+ *  DD_FLAG_DEVICE_INPUT.  cost: DD_COST_SQEUCLID.  eps: FIXED -> the eps of
+ *  the sweeps; LADDER -> the final eps.  cell_size: basic cell side s (power
+ *  of two, n/s even).  The state starts at the coarsest layer with the
+ *  product coupling nu_i = ||mu_i|| nu and alpha = 0 (A3). */
+int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, double eps,
+            int cell_size, const dd_options* opt);
+
+/* dd_iterate -- n_half_iters sweeps A, B, A, ... (Alg. 2 lines 5-14). */
+int dd_iterate(dd_ctx* ctx, int n_half_iters);
+
+/* dd_set_eps -- change eps keeping alpha = eps log u constant. */
+int dd_set_eps(dd_ctx* ctx, double eps);
+
+/* dd_refine -- move to the next finer layer: nu_i^0 by eq. FineBasicMarginals
+ * (P:1471-1474); alpha cold start (reading A14). */
+int dd_refine(dd_ctx* ctx);
+
+/* dd_run_schedule -- LADDER mode: run the whole schedule (refinements, eps
+ * stages, sweeps) asynchronously on the context stream. */
+int dd_run_schedule(dd_ctx* ctx);
+
+/* dd_reset -- return to the initial state (coarsest layer, product coupling). */
+int dd_reset(dd_ctx* ctx);
+
+/* dd_primal_cost -- evaluate the plan pi = sum_J pi_J of the last swept
+ * partition (A if none), each pi_J rebuilt from alpha_{C,J} and
+ * nu_cell = sum_{i in J} nu_i by one Y-iteration (A15):
+ * transport_cost = <c, pi>; entropic = eps (KL(pi|K) - ||K||). */
+int dd_primal_cost(dd_ctx* ctx, double* transport_cost, double* entropic);
+
+/* dd_marginal_error -- l1_x = sum_x |P_X pi(x) - mu(x)| of that plan;
+ * l1_y = sum_y |sum_i nu_i(y) - nu(y)| (A18). */
+int dd_marginal_error(dd_ctx* ctx, double* l1_x, double* l1_y);
+
+/* dd_fetch_plan -- two-call export.
+ *  DD_PLAN_BASIC_MARGINALS: the paper's state: nb*nb int32 boxes
+ *   (y0r, y0c, hr, hc), nb*nb int64 offsets, then fp64 values (row-major per
+ *   box), all packed back to back in buf.
+ *  DD_PLAN_COO: (int32 x, int32 y, fp64 mass) records of the cell plans of
+ *   the last sweep; intended for n <= 256.
+ *  *bytes: in = capacity of buf, out = bytes required/written. */
+int dd_fetch_plan(dd_ctx* ctx, int format, void* buf, size_t* bytes);
+
+/* Statistics: last sweep / totals since init or dd_reset_totals. */
+int dd_get_stats(dd_ctx* ctx, dd_sweep_stats* last);
+int dd_get_totals(dd_ctx* ctx, dd_sweep_stats* totals);
+int dd_reset_totals(dd_ctx* ctx);
+
+/* State export/import for single-sweep parity.  Layout as in
+ * DD_PLAN_BASIC_MARGINALS plus alpha_A, alpha_B (side*side fp64, cost units).
+ * Host buffers; values sized by dd_get_state_info().entries. */
+int dd_get_state_info(dd_ctx* ctx, dd_state_info* info);
+int dd_get_state(dd_ctx* ctx, int* boxes, long long* offsets, double* values,
+                 double* alpha_A, double* alpha_B);
+int dd_set_state(dd_ctx* ctx, int side, long long half_index, int last_partition,
+                 const int* boxes, const long long* offsets, const double* values,
+                 long long n_values, const double* alpha_A, const double* alpha_B);
+
+/* Schedule of the LADDER driver: up to max stages
+ * (side, kappa, sweeps); returns the stage count. */
+int dd_build_schedule(int n_final, int coarsest_side, double kappa_final, double eps_start,
+                      int* side, double* kappa, int* sweeps, int max);
+
+/* Measured MUFU (ex2.approx) throughput of this device in ops/s, and the SM
+ * clock (MHz) the measurement ran at (roofline denominator). */
+int dd_measure_mufu_peak(int device, double* ops_per_s);
+
+int dd_synchronize(dd_ctx* ctx);
+void dd_free(dd_ctx* ctx);
+const char* dd_last_error(const dd_ctx* ctx);
+const char* dd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

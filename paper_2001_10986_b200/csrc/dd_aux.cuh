@@ -1,0 +1,61 @@
+// dd_aux.cuh -- host-visible declarations of the B200 path's kernels.
+#pragma once
+#include "dd_common.cuh"
+
+namespace dd {
+
+struct DevStats {
+    long long cells, iters_sum;
+    int iters_max, failed;
+    double err_sum, mufu;
+    long long fallbacks, deferred;
+    int max_box, overflow;
+    long long entries;
+};
+
+struct EvalParams {
+    int part, side, s, nb, nca;
+    double eps;
+    const int4* box;
+    const long long* off;
+    const double* pool;
+    const double* alpha;
+    const double* mu;
+    const double* logmu;
+    const double* nu;
+    double* scratch;            // per cell: nu_cell[max_ny], g[max_ny], f[max_nx]
+    long long scratch_per_cell;
+    int max_ny;
+    double* cell_res;           // 3 per cell
+    int coo;
+    const long long* coo_off;
+    int* coo_x;
+    int* coo_y;
+    double* coo_m;
+};
+
+size_t k1_smem_bytes_host(int s, int bcap);
+cudaError_t launch_k1(const SweepParams& p, int grid, size_t smem, cudaStream_t st);
+cudaError_t launch_pool2x2(const double* fine, double* coarse, int sc, cudaStream_t st);
+cudaError_t launch_log(const double* x, double* lx, long long n, cudaStream_t st);
+cudaError_t launch_mass_i(const double* mu, double* mass, int side, int s, int nb, cudaStream_t st);
+cudaError_t launch_product_init(int4* box, long long* off, double* pool, const double* mass, const double* nu,
+                                int side, int nb, cudaStream_t st);
+cudaError_t launch_scan_areas(const int4* box, long long* newoff, long long* total, int n, long long* entries,
+                              cudaStream_t st);
+cudaError_t launch_copy_boxes(const int4* box, const long long* srcoff, const long long* dstoff, const double* src,
+                              double* dst, int n, long long cap, cudaStream_t st);
+cudaError_t launch_reduce_stats(const CellOut* out, int ncells, DevStats* last, DevStats* tot,
+                                const long long* entries, const int* n_deferred, const int* overflow,
+                                cudaStream_t st);
+cudaError_t launch_refine(const int4* cbox, const long long* coff, const double* cpool, int4* fbox,
+                          long long* foff, double* fpool, const double* cnu, const double* fnu,
+                          const double* cmass, const double* fmass, int nbc, int nbf, int sidec, int sidef,
+                          long long cap, int* overflow, long long* total, long long* entries, cudaStream_t st);
+cudaError_t launch_scatter_l1y(const int4* box, const long long* off, const double* pool, int nb,
+                               unsigned long long* acc, const double* nu, int side, double* partial,
+                               double* out, cudaStream_t st);
+cudaError_t launch_eval(const EvalParams& p, int ncells, double* sums, cudaStream_t st);
+cudaError_t launch_mufu_bench(float* out, int blocks, int threads, int iters, cudaStream_t st);
+
+}  // namespace dd

@@ -1,0 +1,127 @@
+// dd_common.cuh -- device-side types and helpers of the B200 entropic domain
+// decomposition path (arXiv 2001.10986).  Product code: shares nothing with
+// oracle/.  See DESIGN.md for the numerics (hi/lo split potentials, local
+// affine gauge, speculative stabilisers).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dd {
+
+// ------------------------------------------------------------ constants --
+constexpr float kL2E = 1.4426950408889634f;   // log2(e)
+constexpr float kLN2 = 0.6931471805599453f;
+// hi parts of potentials live on the grid 2^-8: sums
+// and differences of on-grid values of magnitude < 2^15 are exact in fp32.
+constexpr float kGridMagic = 49152.0f;        // 1.5 * 2^15: (v + M) - M rounds v to 2^-8
+constexpr int kThreads = 256;                 // K1 block size
+
+// ------------------------------------------------------------- structs --
+// Per composite cell result of one solve (K1 -> K3).
+struct CellOut {
+    int iters;        // Sinkhorn iterations (Y+X pairs)
+    int flags;        // bit0 no-convergence, bit1 non-finite, bit2 deferred, bit3 overflow
+    float err;        // L1 X-error of the returned plan
+    int box;          // max(b_r, b_c) of the union Y box
+    double mufu;      // MUFU ops executed (ex2 + lg2/rcp), without fallbacks
+    int fallbacks;    // outputs recomputed with an exact max (speculative miss)
+    int pad;
+};
+
+struct SweepParams {
+    int part;             // 1 = A, 2 = B
+    int side, s, nb, nca; // layer side, basic cell side, basic cells/axis, cells/axis of part
+    int ncells;
+    double eps;           // [0,1]^2 units
+    double kappa;         // eps / h^2 (squared pixels)
+    double tau;           // truncation threshold
+    double err_tol;       // Err
+    int max_iter;
+    int bcap;             // max Y-box side this launch handles
+    int mode;             // 0: one CTA per cell (defer big ones); 1: work list
+    int4* box;            // nb*nb (y0r, y0c, hr, hc), updated in place
+    long long* off;       // nb*nb offsets (in: pool_in, out: scratch)
+    const double* pool_in;
+    double* scratch;
+    unsigned long long* bump;   // scratch allocation counter (entries)
+    long long cap;              // scratch capacity (entries)
+    double* alpha;        // alpha_C image, side*side
+    const double* mu;     // layer mu
+    const double* logmu;  // layer log mu (-inf where 0)
+    const double* mass_i; // nb*nb
+    CellOut* out;         // ncells
+    int* deferred;        // list of deferred cell ids
+    int* n_deferred;
+    int* work_counter;    // mode 1 dynamic work index
+    int* overflow;        // set if scratch capacity exceeded
+};
+
+// ------------------------------------------------------------- helpers --
+__device__ __forceinline__ float ex2f(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcpf(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// Round to the 2^-8 grid without touching the XU pipe (two FADDs).
+__device__ __forceinline__ float grid8(float v) {
+    return __fsub_rn(__fadd_rn(v, kGridMagic), kGridMagic);
+}
+__host__ __device__ inline int odd_pitch(int n) { return n | 1; }
+
+// Composite-cell geometry (A11): basic rows/cols of
+// cell p along one axis of partition part.
+__device__ __forceinline__ void cell_span(int nb, int part, int p, int& lo, int& hi) {
+    if (part == 1) { lo = 2 * p; hi = 2 * p + 1; }
+    else {
+        lo = 2 * p - 1 < 0 ? 0 : 2 * p - 1;
+        hi = 2 * p > nb - 1 ? nb - 1 : 2 * p;
+    }
+}
+
+// Block-wide reductions (blockDim.x == kThreads).  red: >= 32 doubles of smem.
+__device__ __forceinline__ double warp_sum(double v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ int warp_min_i(int v) {
+    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ int warp_max_i(int v) {
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+// Fixed-order block sum: every thread returns the total.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    const int nw = blockDim.x >> 5;
+    for (int k = 0; k < nw; ++k) t += red[k];
+    return t;
+}
+__device__ __forceinline__ double block_max(double v, double* red) {
+    v = warp_max(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    double t = -INFINITY;
+    const int nw = blockDim.x >> 5;
+    for (int k = 0; k < nw; ++k) t = fmax(t, red[k]);
+    return t;
+}
+
+}  // namespace dd

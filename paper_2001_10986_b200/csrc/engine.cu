@@ -1,0 +1,855 @@
+// engine.cu -- host side of libdd_gpu.so: the C-ABI of include/dd.h, device
+// memory management, the sweep pipeline (K1 -> K2 -> K3) and the
+// coarse-to-fine / eps-scaling driver.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dd.h"
+#include "dd_aux.cuh"
+
+using namespace dd;
+
+namespace {
+
+constexpr int kMaxLayers = 16;
+
+struct Layer {
+    int side = 0, s = 0, nb = 0;
+    double* mu = nullptr;
+    double* nu = nullptr;
+    double* logmu = nullptr;
+    double* mass = nullptr;
+};
+
+struct SweepEvents {
+    cudaEvent_t e[3];
+};
+
+}  // namespace
+
+struct dd_ctx {
+    dd_options opt{};
+    int device = 0;
+    cudaStream_t st = nullptr;
+    bool own_stream = false;
+    int n_layers = 0, cur = 0;
+    Layer L[kMaxLayers];
+    double eps = 0, eps_final = 0, tau = 1e-15;
+    int cell_size = 0;
+    // state (sized for the finest layer)
+    double* alphaA = nullptr;
+    double* alphaB = nullptr;
+    int4* box = nullptr;
+    int4* box2 = nullptr;
+    long long* off = nullptr;
+    long long* off2 = nullptr;
+    double* pool = nullptr;
+    double* scratch = nullptr;
+    long long cap = 0;
+    // sweep plumbing
+    unsigned long long* bump = nullptr;
+    int* deferred = nullptr;
+    int* counters = nullptr;        // [0] n_deferred, [1] work_counter, [2] overflow
+    CellOut* cellout = nullptr;
+    long long* d_total = nullptr;   // [0] padded pool length, [1] entries
+    DevStats* d_last = nullptr;
+    DevStats* d_tot = nullptr;
+    int ncell_max = 0;
+    int bcap_main = 32, bcap_big = 32;
+    size_t smem_main = 0, smem_big = 0;
+    int grid_big = 148;
+    // evaluation scratch
+    double* eval_scratch = nullptr;
+    size_t eval_scratch_bytes = 0;
+    double* eval_res = nullptr;
+    size_t eval_res_n = 0;
+    double* d_sums = nullptr;       // 4 doubles
+    unsigned long long* yacc = nullptr;
+    double* partial = nullptr;
+    // host bookkeeping
+    long long half_index = 0;
+    int last_part = 0;
+    std::vector<SweepEvents> pending;
+    std::vector<SweepEvents> free_events;
+    double ms_last = 0, solve_ms_last = 0, ms_tot = 0, solve_ms_tot = 0;
+    long long launches_last = 0, launches_tot = 0, launches_pending = 0;
+    std::string err;
+};
+
+namespace {
+
+void set_err(dd_ctx* c, const char* fmt, ...) {
+    if (!c) return;
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    c->err = buf;
+}
+
+#define CK(call)                                                                     \
+    do {                                                                             \
+        cudaError_t _e = (call);                                                     \
+        if (_e != cudaSuccess) {                                                     \
+            set_err(c, "%s: %s (%s:%d)", #call, cudaGetErrorString(_e), __FILE__, __LINE__); \
+            return _e == cudaErrorMemoryAllocation ? DD_ENOMEM : DD_ECUDA;           \
+        }                                                                            \
+    } while (0)
+
+bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+
+int cells_axis(int nb, int part) { return part == 1 ? nb / 2 : nb / 2 + 1; }
+
+// Schedule of P:1553-1561 (A12).  Independent of the oracle's copy.
+int build_schedule(int n_final, int coarsest, double kappa_final, double eps_start, int* side, double* kappa,
+                   int* sweeps, int max) {
+    int k = 0;
+    auto push = [&](int sd, double kk, int w) {
+        if (k < max) { side[k] = sd; kappa[k] = kk; sweeps[k] = w; }
+        ++k;
+    };
+    if (coarsest <= 0) coarsest = 8;
+    if (coarsest > n_final) coarsest = n_final;
+    for (int sd = coarsest; sd <= n_final; sd *= 2) {
+        const bool finest = (sd == n_final);
+        if (sd == coarsest && eps_start > 0.0) {
+            const double ks = eps_start * (double)sd * (double)sd;
+            for (double kk = ks; kk > 2.0 * (1.0 + 1e-12); kk *= 0.5) push(sd, kk, 2);
+        }
+        if (finest && kappa_final > 2.0 * (1.0 + 1e-12)) { push(sd, kappa_final, 4); continue; }
+        push(sd, 2.0, 4);
+        if (!finest) { push(sd, 1.0, 2); push(sd, 0.5, 2); }
+        else
+            for (double kk = 1.0; kk >= kappa_final * (1.0 - 1e-12); kk *= 0.5) push(sd, kk, 2);
+    }
+    return k;
+}
+
+int alloc_events(dd_ctx* c, SweepEvents& ev) {
+    if (!c->free_events.empty()) {
+        ev = c->free_events.back();
+        c->free_events.pop_back();
+        return DD_OK;
+    }
+    for (int k = 0; k < 3; ++k) CK(cudaEventCreate(&ev.e[k]));
+    return DD_OK;
+}
+
+// Harvest the timings of finished sweeps (synchronises the stream).
+int harvest(dd_ctx* c) {
+    CK(cudaStreamSynchronize(c->st));
+    for (auto& ev : c->pending) {
+        float a = 0, b = 0;
+        CK(cudaEventElapsedTime(&a, ev.e[0], ev.e[2]));
+        CK(cudaEventElapsedTime(&b, ev.e[0], ev.e[1]));
+        c->ms_last = a;
+        c->solve_ms_last = b;
+        c->ms_tot += a;
+        c->solve_ms_tot += b;
+        c->free_events.push_back(ev);
+    }
+    c->pending.clear();
+    c->launches_tot += c->launches_pending;
+    c->launches_pending = 0;
+    return DD_OK;
+}
+
+int check_overflow(dd_ctx* c) {
+    int ov = 0;
+    CK(cudaMemcpyAsync(&ov, c->counters + 2, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (ov & 1) {
+        set_err(c, "nu_i pool capacity (%lld entries) exceeded; raise dd_options.pool_capacity", c->cap);
+        return DD_ENOMEM;
+    }
+    if (ov & 2) {
+        set_err(c, "a composite cell's Y box exceeds the largest supported box side (%d)", c->bcap_big);
+        return DD_ENOMEM;
+    }
+    return DD_OK;
+}
+
+void choose_caps(dd_ctx* c, int s) {
+    // main launch: SMEM for boxes up to bcap_main; larger cells go to the big path
+    int want = (s <= 4) ? 24 : 32;
+    if (c->opt.reserved[0] > 0) want = c->opt.reserved[0];
+    if (want < 2 * s + 2) want = 2 * s + 2;
+    c->bcap_main = want;
+    c->smem_main = k1_smem_bytes_host(s, want);
+    int big = want;
+    while (k1_smem_bytes_host(s, big + 1) <= 220 * 1024) ++big;
+    c->bcap_big = big;
+    c->smem_big = k1_smem_bytes_host(s, big);
+}
+
+// One sweep (Alg. 2 lines 6-14) over the partition selected by the parity of
+// the half-iteration index (line 7: odd l -> A).
+int sweep(dd_ctx* c) {
+    Layer& Lr = c->L[c->cur];
+    const int part = (c->half_index % 2 == 0) ? 1 : 2;
+    const int nca = cells_axis(Lr.nb, part);
+    const int ncells = nca * nca;
+    choose_caps(c, Lr.s);
+    CK(cudaMemsetAsync(c->bump, 0, sizeof(unsigned long long), c->st));
+    CK(cudaMemsetAsync(c->counters, 0, 2 * sizeof(int), c->st));
+    SweepParams p{};
+    p.part = part;
+    p.side = Lr.side; p.s = Lr.s; p.nb = Lr.nb; p.nca = nca; p.ncells = ncells;
+    p.eps = c->eps;
+    p.kappa = c->eps * (double)Lr.side * (double)Lr.side;
+    p.tau = c->tau;
+    p.err_tol = c->opt.err_tol;
+    p.max_iter = c->opt.max_inner_iter;
+    p.box = c->box; p.off = c->off;
+    p.pool_in = c->pool; p.scratch = c->scratch; p.bump = c->bump; p.cap = c->cap;
+    p.alpha = part == 1 ? c->alphaA : c->alphaB;
+    p.mu = Lr.mu; p.logmu = Lr.logmu; p.mass_i = Lr.mass;
+    p.out = c->cellout;
+    p.deferred = c->deferred; p.n_deferred = c->counters; p.work_counter = c->counters + 1;
+    p.overflow = c->counters + 2;
+    SweepEvents ev;
+    int rc = alloc_events(c, ev);
+    if (rc) return rc;
+    CK(cudaEventRecord(ev.e[0], c->st));
+    p.mode = 0; p.bcap = c->bcap_main;
+    CK(launch_k1(p, ncells, c->smem_main, c->st));
+    p.mode = 1; p.bcap = c->bcap_big;
+    CK(launch_k1(p, std::min(c->grid_big, ncells), c->smem_big, c->st));
+    CK(cudaEventRecord(ev.e[1], c->st));
+    // K2: deterministic compaction of the new boxes into the pool
+    const int nb2 = Lr.nb * Lr.nb;
+    CK(launch_scan_areas(c->box, c->off2, c->d_total, nb2, c->d_total + 1, c->st));
+    CK(launch_copy_boxes(c->box, c->off, c->off2, c->scratch, c->pool, nb2, c->cap, c->st));
+    std::swap(c->off, c->off2);
+    // K3: fixed-order sweep statistics
+    CK(launch_reduce_stats(c->cellout, ncells, c->d_last, c->d_tot, c->d_total + 1, c->counters,
+                           c->counters + 2, c->st));
+    CK(cudaEventRecord(ev.e[2], c->st));
+    c->pending.push_back(ev);
+    c->launches_pending += 5;
+    c->half_index++;
+    c->last_part = part;
+    if (c->pending.size() > 512) return harvest(c);
+    return DD_OK;
+}
+
+int product_init(dd_ctx* c) {
+    Layer& Lr = c->L[c->cur];
+    const long long need = (long long)Lr.nb * Lr.nb * Lr.side * Lr.side;
+    if (need > c->cap) { set_err(c, "pool capacity too small for the product initialisation"); return DD_ENOMEM; }
+    CK(launch_product_init(c->box, c->off, c->pool, Lr.mass, Lr.nu, Lr.side, Lr.nb, c->st));
+    const size_t n2 = (size_t)c->L[c->n_layers - 1].side * c->L[c->n_layers - 1].side;
+    CK(cudaMemsetAsync(c->alphaA, 0, n2 * sizeof(double), c->st));
+    CK(cudaMemsetAsync(c->alphaB, 0, n2 * sizeof(double), c->st));
+    CK(cudaMemsetAsync(c->counters, 0, 3 * sizeof(int), c->st));
+    c->half_index = 0;
+    c->last_part = 0;
+    return DD_OK;
+}
+
+void free_all(dd_ctx* c) {
+    for (int k = 0; k < c->n_layers; ++k) {
+        cudaFree(c->L[k].mu); cudaFree(c->L[k].nu); cudaFree(c->L[k].logmu); cudaFree(c->L[k].mass);
+    }
+    void* ptrs[] = {c->alphaA, c->alphaB, c->box, c->box2, c->off, c->off2, c->pool, c->scratch,
+                    c->bump, c->deferred, c->counters, c->cellout, c->d_total, c->d_last, c->d_tot,
+                    c->eval_scratch, c->eval_res, c->d_sums, c->yacc, c->partial};
+    for (void* q : ptrs) if (q) cudaFree(q);
+    for (auto& ev : c->pending) for (int k = 0; k < 3; ++k) cudaEventDestroy(ev.e[k]);
+    for (auto& ev : c->free_events) for (int k = 0; k < 3; ++k) cudaEventDestroy(ev.e[k]);
+    if (c->own_stream && c->st) cudaStreamDestroy(c->st);
+}
+
+// Evaluate the plan of the last swept partition (K7) -> sums[0..2] = cost, ent, l1x.
+int evaluate(dd_ctx* c, double* out3, bool coo, long long* coo_count, int* cx, int* cy, double* cm) {
+    Layer& Lr = c->L[c->cur];
+    const int part = c->last_part ? c->last_part : 1;
+    const int nca = cells_axis(Lr.nb, part);
+    const int ncells = nca * nca;
+    const int nb2 = Lr.nb * Lr.nb;
+    std::vector<int4> hbox(nb2);
+    CK(cudaMemcpyAsync(hbox.data(), c->box, nb2 * sizeof(int4), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    // per-cell union boxes on the host (sizes only) for scratch / COO layout
+    std::vector<long long> coo_off(ncells + 1, 0);
+    int max_ny = 1;
+    const int nx_max = 4 * Lr.s * Lr.s;
+    for (int cell = 0; cell < ncells; ++cell) {
+        const int cp = cell / nca, cq = cell % nca;
+        int rlo, rhi, clo, chi;
+        auto span = [&](int q, int& lo, int& hi) {
+            if (part == 1) { lo = 2 * q; hi = 2 * q + 1; }
+            else { lo = std::max(2 * q - 1, 0); hi = std::min(2 * q, Lr.nb - 1); }
+        };
+        span(cp, rlo, rhi);
+        span(cq, clo, chi);
+        int y0 = 1 << 30, x0 = 1 << 30, y1 = -1, x1 = -1;
+        for (int r = rlo; r <= rhi; ++r)
+            for (int q = clo; q <= chi; ++q) {
+                const int4 b = hbox[r * Lr.nb + q];
+                if (b.z <= 0 || b.w <= 0) continue;
+                y0 = std::min(y0, b.x); x0 = std::min(x0, b.y);
+                y1 = std::max(y1, b.x + b.z - 1); x1 = std::max(x1, b.y + b.w - 1);
+            }
+        const int ny = y1 >= 0 ? (y1 - y0 + 1) * (x1 - x0 + 1) : 0;
+        max_ny = std::max(max_ny, ny);
+        const int nx = (rhi - rlo + 1) * (chi - clo + 1) * Lr.s * Lr.s;
+        coo_off[cell + 1] = coo_off[cell] + (long long)nx * ny;
+    }
+    const long long per_cell = 2LL * max_ny + nx_max;
+    const size_t need = (size_t)per_cell * ncells * sizeof(double);
+    if (need > c->eval_scratch_bytes) {
+        if (c->eval_scratch) cudaFree(c->eval_scratch);
+        c->eval_scratch = nullptr;
+        CK(cudaMalloc(&c->eval_scratch, need));
+        c->eval_scratch_bytes = need;
+    }
+    if ((size_t)3 * ncells > c->eval_res_n) {
+        if (c->eval_res) cudaFree(c->eval_res);
+        c->eval_res = nullptr;
+        CK(cudaMalloc(&c->eval_res, 3 * ncells * sizeof(double)));
+        c->eval_res_n = 3 * ncells;
+    }
+    EvalParams p{};
+    p.part = part; p.side = Lr.side; p.s = Lr.s; p.nb = Lr.nb; p.nca = nca;
+    p.eps = c->eps;
+    p.box = c->box; p.off = c->off; p.pool = c->pool;
+    p.alpha = part == 1 ? c->alphaA : c->alphaB;
+    p.mu = Lr.mu; p.logmu = Lr.logmu; p.nu = Lr.nu;
+    p.scratch = c->eval_scratch; p.scratch_per_cell = per_cell; p.max_ny = max_ny;
+    p.cell_res = c->eval_res;
+    long long* d_coo_off = nullptr;
+    int* dx = nullptr;
+    int* dy = nullptr;
+    double* dm = nullptr;
+    const long long total = coo_off[ncells];
+    if (coo) {
+        if (coo_count) *coo_count = total;
+        if (!cx) return DD_OK;   // size query
+        CK(cudaMalloc(&d_coo_off, (ncells + 1) * sizeof(long long)));
+        CK(cudaMalloc(&dx, std::max(1LL, total) * sizeof(int)));
+        CK(cudaMalloc(&dy, std::max(1LL, total) * sizeof(int)));
+        CK(cudaMalloc(&dm, std::max(1LL, total) * sizeof(double)));
+        CK(cudaMemcpyAsync(d_coo_off, coo_off.data(), (ncells + 1) * sizeof(long long), cudaMemcpyHostToDevice, c->st));
+        p.coo = 1; p.coo_off = d_coo_off; p.coo_x = dx; p.coo_y = dy; p.coo_m = dm;
+    }
+    CK(launch_eval(p, ncells, c->d_sums, c->st));
+    CK(cudaMemcpyAsync(out3, c->d_sums, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    if (coo) {
+        CK(cudaMemcpyAsync(cx, dx, total * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(cy, dy, total * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(cm, dm, total * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    }
+    CK(cudaStreamSynchronize(c->st));
+    if (coo) { cudaFree(d_coo_off); cudaFree(dx); cudaFree(dy); cudaFree(dm); }
+    return DD_OK;
+}
+
+void fill_stats(const DevStats& d, dd_sweep_stats* s) {
+    s->cells = d.cells;
+    s->iters_sum = d.iters_sum;
+    s->iters_max = d.iters_max;
+    s->failed = d.failed;
+    s->err_x_sum = d.err_sum;
+    s->entries = d.entries;
+    s->mufu_ops = d.mufu;
+    s->big_cells = d.deferred;
+    s->max_box = d.max_box;
+    s->reserved_i = (int)std::min<long long>(d.fallbacks, 2147483647LL);
+}
+
+}  // namespace
+
+// =================================================================== ABI ==
+extern "C" {
+
+const char* dd_version(void) { return "ddot-b200 0.1 (sm_100a)"; }
+
+const char* dd_last_error(const dd_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int dd_build_schedule(int n_final, int coarsest_side, double kappa_final, double eps_start, int* side,
+                      double* kappa, int* sweeps, int max) {
+    return build_schedule(n_final, coarsest_side, kappa_final, eps_start, side, kappa, sweeps, max);
+}
+
+int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, double eps, int cell_size,
+            const dd_options* opt) {
+    if (!out) return DD_EINVAL;
+    *out = nullptr;
+    dd_ctx* c = new (std::nothrow) dd_ctx();
+    if (!c) return DD_ENOMEM;
+    *out = c;
+    if (opt) c->opt = *opt;
+    if (c->opt.err_tol <= 0) c->opt.err_tol = 1e-6;
+    if (c->opt.max_inner_iter <= 0) c->opt.max_inner_iter = 10000;
+    c->tau = c->opt.trunc_tau == 0.0 ? 1e-15 : (c->opt.trunc_tau < 0 ? 0.0 : c->opt.trunc_tau);
+    if (c->opt.no_truncate) c->tau = 0.0;
+    if (cost != DD_COST_SQEUCLID) { set_err(c, "only DD_COST_SQEUCLID is supported"); return DD_EINVAL; }
+    if (!is_pow2(n) || n < 4) { set_err(c, "n=%d must be a power of two >= 4", n); return DD_EINVAL; }
+    if (!is_pow2(cell_size) || cell_size > n / 2 || (n / cell_size) % 2) {
+        set_err(c, "cell_size=%d must be a power of two with n/s even", cell_size);
+        return DD_EINVAL;
+    }
+    if (!(eps > 0.0) || !std::isfinite(eps)) { set_err(c, "eps must be > 0"); return DD_EINVAL; }
+    if (!mu || !nu) { set_err(c, "null marginal"); return DD_EINVAL; }
+    // ---- device
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        set_err(c, "no CUDA device: this library has no CPU fallback");
+        return DD_ECUDA;
+    }
+    c->device = c->opt.device;
+    CK(cudaSetDevice(c->device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, c->device));
+    if (prop.major < 10) {
+        set_err(c, "device %s (sm_%d%d) is not sm_100: this build targets B200 only", prop.name, prop.major, prop.minor);
+        return DD_ECUDA;
+    }
+    c->grid_big = prop.multiProcessorCount;
+    if (c->opt.stream) c->st = (cudaStream_t)c->opt.stream;
+    else {
+        CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    // ---- host validation (every basic cell of every layer has mass > 0)
+    const size_t n2 = (size_t)n * n;
+    std::vector<double> hmu(n2), hnu(n2);
+    if (c->opt.flags & DD_FLAG_DEVICE_INPUT) {
+        CK(cudaMemcpy(hmu.data(), mu, n2 * sizeof(double), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(hnu.data(), nu, n2 * sizeof(double), cudaMemcpyDeviceToHost));
+    } else {
+        memcpy(hmu.data(), mu, n2 * sizeof(double));
+        memcpy(hnu.data(), nu, n2 * sizeof(double));
+    }
+    double smu = 0, snu = 0;
+    for (size_t k = 0; k < n2; ++k) {
+        if (!std::isfinite(hmu[k]) || hmu[k] < 0 || !std::isfinite(hnu[k]) || hnu[k] < 0) {
+            set_err(c, "marginals must be finite and >= 0 (index %zu)", k);
+            return DD_EINVAL;
+        }
+        smu += hmu[k];
+        snu += hnu[k];
+    }
+    if (!(smu > 0) || std::fabs(smu - snu) > 1e-12 * smu) {
+        set_err(c, "||mu|| = %.17g != ||nu|| = %.17g", smu, snu);
+        return DD_EINVAL;
+    }
+    int coarsest = n;
+    if (c->opt.schedule == DD_SCHED_LADDER) {
+        coarsest = c->opt.coarsest_side > 0 ? c->opt.coarsest_side : 8;
+        if (!is_pow2(coarsest) || coarsest < 4) { set_err(c, "bad coarsest_side"); return DD_EINVAL; }
+        coarsest = std::min(coarsest, n);
+    }
+    int nl = 0;
+    for (int sd = coarsest; sd <= n; sd *= 2) ++nl;
+    if (nl > kMaxLayers) { set_err(c, "too many layers"); return DD_EINVAL; }
+    c->n_layers = nl;
+    c->cell_size = cell_size;
+    {   // host-side basic-cell masses per layer (validation only)
+        std::vector<double> m = hmu;
+        int sd = n;
+        for (int k = nl - 1; k >= 0; --k) {
+            const int s = std::min(cell_size, sd / 2), nb = sd / s;
+            std::vector<double> mass((size_t)nb * nb, 0.0);
+            for (int i = 0; i < sd; ++i)
+                for (int j = 0; j < sd; ++j) mass[(i / s) * nb + j / s] += m[(size_t)i * sd + j];
+            for (int q = 0; q < nb * nb; ++q)
+                if (!(mass[q] > 0)) {
+                    set_err(c, "basic cell %d of layer side %d has zero mass (P:299)", q, sd);
+                    return DD_EINVAL;
+                }
+            if (k > 0) {
+                std::vector<double> cm((size_t)(sd / 2) * (sd / 2));
+                for (int i = 0; i < sd / 2; ++i)
+                    for (int j = 0; j < sd / 2; ++j) {
+                        const size_t a = (size_t)(2 * i) * sd + 2 * j;
+                        cm[(size_t)i * (sd / 2) + j] = (m[a] + m[a + 1]) + (m[a + sd] + m[a + sd + 1]);
+                    }
+                m.swap(cm);
+                sd /= 2;
+            }
+        }
+    }
+    // ---- device layers: finest uploaded, coarser by 2x2 sum pooling (A20)
+    for (int k = nl - 1; k >= 0; --k) {
+        Layer& Lr = c->L[k];
+        Lr.side = coarsest << k;
+        Lr.s = std::min(cell_size, Lr.side / 2);
+        Lr.nb = Lr.side / Lr.s;
+        const size_t m2 = (size_t)Lr.side * Lr.side;
+        CK(cudaMalloc(&Lr.mu, m2 * sizeof(double)));
+        CK(cudaMalloc(&Lr.nu, m2 * sizeof(double)));
+        CK(cudaMalloc(&Lr.logmu, m2 * sizeof(double)));
+        CK(cudaMalloc(&Lr.mass, (size_t)Lr.nb * Lr.nb * sizeof(double)));
+        if (k == nl - 1) {
+            const cudaMemcpyKind kind = (c->opt.flags & DD_FLAG_DEVICE_INPUT) ? cudaMemcpyDeviceToDevice
+                                                                              : cudaMemcpyHostToDevice;
+            CK(cudaMemcpyAsync(Lr.mu, mu, m2 * sizeof(double), kind, c->st));
+            CK(cudaMemcpyAsync(Lr.nu, nu, m2 * sizeof(double), kind, c->st));
+        } else {
+            CK(launch_pool2x2(c->L[k + 1].mu, Lr.mu, Lr.side, c->st));
+            CK(launch_pool2x2(c->L[k + 1].nu, Lr.nu, Lr.side, c->st));
+        }
+        CK(launch_log(Lr.mu, Lr.logmu, (long long)m2, c->st));
+        CK(launch_mass_i(Lr.mu, Lr.mass, Lr.side, Lr.s, Lr.nb, c->st));
+    }
+    // ---- state buffers (finest sizes)
+    const Layer& F = c->L[nl - 1];
+    const Layer& C0 = c->L[0];
+    const int nbmax = F.nb;
+    c->cap = c->opt.pool_capacity > 0 ? c->opt.pool_capacity : 64LL * (long long)n2 + (1LL << 22);
+    c->cap = std::max(c->cap, (long long)C0.nb * C0.nb * C0.side * C0.side + 16);
+    CK(cudaMalloc(&c->alphaA, n2 * sizeof(double)));
+    CK(cudaMalloc(&c->alphaB, n2 * sizeof(double)));
+    CK(cudaMalloc(&c->box, (size_t)nbmax * nbmax * sizeof(int4)));
+    CK(cudaMalloc(&c->box2, (size_t)nbmax * nbmax * sizeof(int4)));
+    CK(cudaMalloc(&c->off, (size_t)nbmax * nbmax * sizeof(long long)));
+    CK(cudaMalloc(&c->off2, (size_t)nbmax * nbmax * sizeof(long long)));
+    CK(cudaMalloc(&c->pool, (size_t)c->cap * sizeof(double)));
+    CK(cudaMalloc(&c->scratch, (size_t)c->cap * sizeof(double)));
+    CK(cudaMalloc(&c->bump, sizeof(unsigned long long)));
+    c->ncell_max = (nbmax / 2 + 1) * (nbmax / 2 + 1);
+    CK(cudaMalloc(&c->deferred, (size_t)c->ncell_max * sizeof(int)));
+    CK(cudaMalloc(&c->counters, 4 * sizeof(int)));
+    CK(cudaMalloc(&c->cellout, (size_t)c->ncell_max * sizeof(CellOut)));
+    CK(cudaMalloc(&c->d_total, 2 * sizeof(long long)));
+    CK(cudaMalloc(&c->d_last, sizeof(DevStats)));
+    CK(cudaMalloc(&c->d_tot, sizeof(DevStats)));
+    CK(cudaMalloc(&c->d_sums, 4 * sizeof(double)));
+    CK(cudaMalloc(&c->yacc, n2 * sizeof(unsigned long long)));
+    CK(cudaMalloc(&c->partial, 256 * sizeof(double)));
+    CK(cudaMemsetAsync(c->d_last, 0, sizeof(DevStats), c->st));
+    CK(cudaMemsetAsync(c->d_tot, 0, sizeof(DevStats), c->st));
+    CK(cudaMemsetAsync(c->d_total, 0, 2 * sizeof(long long), c->st));
+    // K1 needs > 48 KB dynamic SMEM on the big path: set the attribute once here
+    choose_caps(c, F.s);
+    c->cur = 0;
+    c->eps_final = eps;
+    c->eps = (c->opt.schedule == DD_SCHED_LADDER) ? 2.0 / ((double)coarsest * coarsest) : eps;
+    int rc = product_init(c);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(c->st));
+    return DD_OK;
+}
+
+int dd_reset(dd_ctx* c) {
+    if (!c) return DD_EINVAL;
+    c->cur = 0;
+    c->eps = (c->opt.schedule == DD_SCHED_LADDER) ? 2.0 / ((double)c->L[0].side * c->L[0].side) : c->eps_final;
+    return product_init(c);
+}
+
+int dd_set_eps(dd_ctx* c, double eps) {
+    if (!c || !(eps > 0.0)) return DD_EINVAL;
+    c->eps = eps;   // alpha = eps log u kept constant
+    return DD_OK;
+}
+
+int dd_iterate(dd_ctx* c, int k) {
+    if (!c || k < 0) return DD_EINVAL;
+    for (int i = 0; i < k; ++i) {
+        int rc = sweep(c);
+        if (rc) return rc;
+    }
+    return DD_OK;
+}
+
+int dd_refine(dd_ctx* c) {
+    if (!c) return DD_EINVAL;
+    if (c->cur + 1 >= c->n_layers) { set_err(c, "already at the finest layer"); return DD_EINVAL; }
+    Layer& Lc = c->L[c->cur];
+    Layer& Lf = c->L[c->cur + 1];
+    CK(launch_refine(c->box, c->off, c->pool, c->box2, c->off2, c->scratch, Lc.nu, Lf.nu, Lc.mass, Lf.mass,
+                     Lc.nb, Lf.nb, Lc.side, Lf.side, c->cap, c->counters + 2, c->d_total, c->d_total + 1, c->st));
+    std::swap(c->box, c->box2);
+    std::swap(c->off, c->off2);
+    std::swap(c->pool, c->scratch);
+    const size_t n2 = (size_t)Lf.side * Lf.side;
+    CK(cudaMemsetAsync(c->alphaA, 0, n2 * sizeof(double), c->st));   // cold start (A14)
+    CK(cudaMemsetAsync(c->alphaB, 0, n2 * sizeof(double), c->st));
+    c->launches_pending += 3;
+    c->cur += 1;
+    c->last_part = 0;
+    return DD_OK;
+}
+
+int dd_run_schedule(dd_ctx* c) {
+    if (!c) return DD_EINVAL;
+    if (c->opt.schedule != DD_SCHED_LADDER) { set_err(c, "dd_run_schedule needs DD_SCHED_LADDER"); return DD_EINVAL; }
+    const int nf = c->L[c->n_layers - 1].side;
+    const double kf = c->eps_final * (double)nf * nf;
+    int sides[256], sweeps[256];
+    double kap[256];
+    const int ns = std::min(256, build_schedule(nf, c->L[0].side, kf, c->opt.eps_start, sides, kap, sweeps, 256));
+    for (int k = 0; k < ns; ++k) {
+        while (c->L[c->cur].side < sides[k]) {
+            int rc = dd_refine(c);
+            if (rc) return rc;
+        }
+        const double h = 1.0 / sides[k];
+        dd_set_eps(c, kap[k] * h * h);
+        int rc = dd_iterate(c, sweeps[k]);
+        if (rc) return rc;
+    }
+    return DD_OK;
+}
+
+int dd_synchronize(dd_ctx* c) {
+    if (!c) return DD_EINVAL;
+    int rc = harvest(c);
+    if (rc) return rc;
+    return check_overflow(c);
+}
+
+int dd_get_stats(dd_ctx* c, dd_sweep_stats* s) {
+    if (!c || !s) return DD_EINVAL;
+    int rc = dd_synchronize(c);
+    if (rc) return rc;
+    DevStats d;
+    CK(cudaMemcpy(&d, c->d_last, sizeof(DevStats), cudaMemcpyDeviceToHost));
+    memset(s, 0, sizeof(*s));
+    fill_stats(d, s);
+    s->ms = c->ms_last;
+    s->solve_ms = c->solve_ms_last;
+    s->launches = 5;
+    if (d.failed) {
+        set_err(c, "%d cells did not converge within max_inner_iter", d.failed);
+        return DD_ENOCONV;
+    }
+    return DD_OK;
+}
+
+int dd_get_totals(dd_ctx* c, dd_sweep_stats* s) {
+    if (!c || !s) return DD_EINVAL;
+    int rc = dd_synchronize(c);
+    if (rc) return rc;
+    DevStats d;
+    CK(cudaMemcpy(&d, c->d_tot, sizeof(DevStats), cudaMemcpyDeviceToHost));
+    memset(s, 0, sizeof(*s));
+    fill_stats(d, s);
+    s->ms = c->ms_tot;
+    s->solve_ms = c->solve_ms_tot;
+    s->launches = c->launches_tot;
+    return DD_OK;
+}
+
+int dd_reset_totals(dd_ctx* c) {
+    if (!c) return DD_EINVAL;
+    int rc = harvest(c);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(c->d_tot, 0, sizeof(DevStats), c->st));
+    CK(cudaStreamSynchronize(c->st));
+    c->ms_tot = c->solve_ms_tot = 0;
+    c->launches_tot = 0;
+    return DD_OK;
+}
+
+int dd_primal_cost(dd_ctx* c, double* transport_cost, double* entropic) {
+    if (!c) return DD_EINVAL;
+    int rc = dd_synchronize(c);
+    if (rc) return rc;
+    double s[3];
+    rc = evaluate(c, s, false, nullptr, nullptr, nullptr, nullptr);
+    if (rc) return rc;
+    if (transport_cost) *transport_cost = s[0];
+    if (entropic) *entropic = s[1];
+    return DD_OK;
+}
+
+int dd_marginal_error(dd_ctx* c, double* l1_x, double* l1_y) {
+    if (!c) return DD_EINVAL;
+    int rc = dd_synchronize(c);
+    if (rc) return rc;
+    double s[3];
+    rc = evaluate(c, s, false, nullptr, nullptr, nullptr, nullptr);
+    if (rc) return rc;
+    Layer& Lr = c->L[c->cur];
+    CK(launch_scatter_l1y(c->box, c->off, c->pool, Lr.nb, c->yacc, Lr.nu, Lr.side, c->partial, c->d_sums + 3, c->st));
+    double ly = 0;
+    CK(cudaMemcpyAsync(&ly, c->d_sums + 3, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (l1_x) *l1_x = s[2];
+    if (l1_y) *l1_y = ly;
+    return DD_OK;
+}
+
+int dd_get_state_info(dd_ctx* c, dd_state_info* info) {
+    if (!c || !info) return DD_EINVAL;
+    int rc = dd_synchronize(c);
+    if (rc) return rc;
+    Layer& Lr = c->L[c->cur];
+    info->side = Lr.side;
+    info->s = Lr.s;
+    info->nb = Lr.nb;
+    info->last_partition = c->last_part;
+    info->half_index = c->half_index;
+    info->eps = c->eps;
+    std::vector<int4> hb((size_t)Lr.nb * Lr.nb);
+    CK(cudaMemcpy(hb.data(), c->box, hb.size() * sizeof(int4), cudaMemcpyDeviceToHost));
+    long long e = 0;
+    for (auto& b : hb) e += (long long)b.z * b.w;
+    info->entries = e;
+    return DD_OK;
+}
+
+int dd_get_state(dd_ctx* c, int* boxes, long long* offsets, double* values, double* alpha_A, double* alpha_B) {
+    if (!c) return DD_EINVAL;
+    int rc = dd_synchronize(c);
+    if (rc) return rc;
+    Layer& Lr = c->L[c->cur];
+    const int nb2 = Lr.nb * Lr.nb;
+    std::vector<int4> hb(nb2);
+    std::vector<long long> ho(nb2);
+    CK(cudaMemcpy(hb.data(), c->box, nb2 * sizeof(int4), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ho.data(), c->off, nb2 * sizeof(long long), cudaMemcpyDeviceToHost));
+    long long o = 0;
+    for (int i = 0; i < nb2; ++i) {
+        const long long a = (long long)hb[i].z * hb[i].w;
+        if (boxes) { boxes[4 * i] = hb[i].x; boxes[4 * i + 1] = hb[i].y; boxes[4 * i + 2] = hb[i].z; boxes[4 * i + 3] = hb[i].w; }
+        if (offsets) offsets[i] = o;
+        if (values && a) CK(cudaMemcpy(values + o, c->pool + ho[i], a * sizeof(double), cudaMemcpyDeviceToHost));
+        o += a;
+    }
+    const size_t n2 = (size_t)Lr.side * Lr.side;
+    if (alpha_A) CK(cudaMemcpy(alpha_A, c->alphaA, n2 * sizeof(double), cudaMemcpyDeviceToHost));
+    if (alpha_B) CK(cudaMemcpy(alpha_B, c->alphaB, n2 * sizeof(double), cudaMemcpyDeviceToHost));
+    return DD_OK;
+}
+
+int dd_set_state(dd_ctx* c, int side, long long half_index, int last_partition, const int* boxes,
+                 const long long* offsets, const double* values, long long n_values, const double* alpha_A,
+                 const double* alpha_B) {
+    if (!c || !boxes || !offsets || !values) return DD_EINVAL;
+    int k = 0;
+    while (k < c->n_layers && c->L[k].side != side) ++k;
+    if (k == c->n_layers) { set_err(c, "no layer of side %d", side); return DD_EINVAL; }
+    int rc = harvest(c);
+    if (rc) return rc;
+    Layer& Lr = c->L[k];
+    const int nb2 = Lr.nb * Lr.nb;
+    std::vector<int4> hb(nb2);
+    std::vector<long long> ho(nb2);
+    long long o = 0;
+    for (int i = 0; i < nb2; ++i) {
+        hb[i] = make_int4(boxes[4 * i], boxes[4 * i + 1], boxes[4 * i + 2], boxes[4 * i + 3]);
+        if (hb[i].z < 0 || hb[i].w < 0 || hb[i].x < 0 || hb[i].y < 0 || hb[i].x + hb[i].z > side ||
+            hb[i].y + hb[i].w > side) {
+            set_err(c, "box %d out of range", i);
+            return DD_EINVAL;
+        }
+        const long long a = (long long)hb[i].z * hb[i].w;
+        if (offsets[i] < 0 || offsets[i] + a > n_values) { set_err(c, "offset %d out of range", i); return DD_EINVAL; }
+        ho[i] = o;
+        o += (a + 1) & ~1LL;
+    }
+    if (o > c->cap) { set_err(c, "state larger than the pool capacity"); return DD_ENOMEM; }
+    std::vector<double> pool(std::max(1LL, o), 0.0);
+    for (int i = 0; i < nb2; ++i) {
+        const long long a = (long long)hb[i].z * hb[i].w;
+        if (a) memcpy(pool.data() + ho[i], values + offsets[i], a * sizeof(double));
+    }
+    CK(cudaMemcpy(c->box, hb.data(), nb2 * sizeof(int4), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->off, ho.data(), nb2 * sizeof(long long), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->pool, pool.data(), pool.size() * sizeof(double), cudaMemcpyHostToDevice));
+    const size_t n2 = (size_t)side * side;
+    if (alpha_A) CK(cudaMemcpy(c->alphaA, alpha_A, n2 * sizeof(double), cudaMemcpyHostToDevice));
+    else CK(cudaMemset(c->alphaA, 0, n2 * sizeof(double)));
+    if (alpha_B) CK(cudaMemcpy(c->alphaB, alpha_B, n2 * sizeof(double), cudaMemcpyHostToDevice));
+    else CK(cudaMemset(c->alphaB, 0, n2 * sizeof(double)));
+    c->cur = k;
+    c->half_index = half_index;
+    c->last_part = last_partition;
+    return DD_OK;
+}
+
+int dd_fetch_plan(dd_ctx* c, int format, void* buf, size_t* bytes) {
+    if (!c || !bytes) return DD_EINVAL;
+    int rc = dd_synchronize(c);
+    if (rc) return rc;
+    Layer& Lr = c->L[c->cur];
+    if (format == DD_PLAN_BASIC_MARGINALS) {
+        dd_state_info info;
+        rc = dd_get_state_info(c, &info);
+        if (rc) return rc;
+        const int nb2 = Lr.nb * Lr.nb;
+        const size_t need = (size_t)nb2 * 4 * sizeof(int) + (size_t)nb2 * sizeof(long long) +
+                            (size_t)info.entries * sizeof(double);
+        if (!buf) { *bytes = need; return DD_OK; }
+        if (*bytes < need) { set_err(c, "buffer too small (%zu < %zu)", *bytes, need); return DD_EINVAL; }
+        char* p = (char*)buf;
+        int* bx = (int*)p;
+        long long* of = (long long*)(p + (size_t)nb2 * 4 * sizeof(int));
+        double* v = (double*)(p + (size_t)nb2 * 4 * sizeof(int) + (size_t)nb2 * sizeof(long long));
+        rc = dd_get_state(c, bx, of, v, nullptr, nullptr);
+        *bytes = need;
+        return rc;
+    }
+    if (format == DD_PLAN_COO) {
+        long long cnt = 0;
+        double s3[3];
+        rc = evaluate(c, s3, true, &cnt, nullptr, nullptr, nullptr);
+        if (rc) return rc;
+        const size_t need = (size_t)cnt * (2 * sizeof(int) + sizeof(double));
+        if (!buf) { *bytes = need; return DD_OK; }
+        if (*bytes < need) { set_err(c, "buffer too small"); return DD_EINVAL; }
+        char* p = (char*)buf;
+        int* xs = (int*)p;
+        int* ys = (int*)(p + cnt * sizeof(int));
+        double* ms = (double*)(p + 2 * cnt * sizeof(int));
+        rc = evaluate(c, s3, true, &cnt, xs, ys, ms);
+        *bytes = need;
+        return rc;
+    }
+    set_err(c, "unknown plan format %d", format);
+    return DD_EINVAL;
+}
+
+int dd_measure_mufu_peak(int device, double* ops_per_s) {
+    if (!ops_per_s) return DD_EINVAL;
+    if (cudaSetDevice(device) != cudaSuccess) return DD_ECUDA;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return DD_ECUDA;
+    float* out = nullptr;
+    if (cudaMalloc(&out, 65536 * sizeof(float)) != cudaSuccess) return DD_ECUDA;
+    cudaStream_t st;
+    cudaStreamCreate(&st);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const int blocks = prop.multiProcessorCount * 8, threads = 256, iters = 4096;
+    double best = 0;
+    for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(a, st);
+        launch_mufu_bench(out, blocks, threads, iters, st);
+        cudaEventRecord(b, st);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        const double ops = (double)blocks * threads * iters * 8.0;
+        if (rep > 0) best = std::max(best, ops / (ms * 1e-3));
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaStreamDestroy(st);
+    cudaFree(out);
+    *ops_per_s = best;
+    return cudaGetLastError() == cudaSuccess ? DD_OK : DD_ECUDA;
+}
+
+void dd_free(dd_ctx* c) {
+    if (!c) return;
+    if (c->st) cudaStreamSynchronize(c->st);
+    free_all(c);
+    delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,469 @@
+// k_aux.cu -- the kernels around K1 (arXiv 2001.10986 Algorithm 2 driver):
+//   layer pyramid, product initialisation, K2 compaction of
+//   the truncated basic-cell marginals, K3 fixed-order sweep
+//   reduction, K4 coarse-to-fine refinement (eq.
+//   FineBasicMarginals), K6 Y-marginal scatter (A18), K7 fp64
+//   primal evaluation (Lemma ScalingKL), and the MUFU
+//   throughput microbenchmark used as the roofline denominator.
+#include "dd_aux.cuh"
+
+namespace dd {
+
+// ---------------------------------------------------------------- pyramid --
+__global__ void k_pool2x2(const double* __restrict__ fine, double* __restrict__ coarse, int sc) {
+    const int n = sc * sc;
+    const int sf = 2 * sc;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int i = k / sc, j = k % sc;
+        const long long a = (long long)(2 * i) * sf + 2 * j;
+        coarse[k] = (fine[a] + fine[a + 1]) + (fine[a + sf] + fine[a + sf + 1]);
+    }
+}
+
+__global__ void k_log(const double* __restrict__ x, double* __restrict__ lx, long long n) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+        lx[k] = x[k] > 0.0 ? log(x[k]) : -INFINITY;
+}
+
+// ||mu_i|| per basic cell, fixed-order block reduction (one block per cell).
+__global__ void k_mass_i(const double* __restrict__ mu, double* __restrict__ mass, int side, int s, int nb) {
+    __shared__ double red[32];
+    const int i = blockIdx.x;
+    const int r0 = (i / nb) * s, c0 = (i % nb) * s;
+    double v = 0.0;
+    for (int k = threadIdx.x; k < s * s; k += blockDim.x)
+        v += mu[(long long)(r0 + k / s) * side + (c0 + k % s)];
+    v = block_sum(v, red);
+    if (threadIdx.x == 0) mass[i] = v;
+}
+
+// Product coupling nu_i^0 = ||mu_i|| nu on the full image (A3).
+__global__ void k_product_init(int4* box, long long* off, double* pool, const double* __restrict__ mass,
+                               const double* __restrict__ nu, int side) {
+    const int i = blockIdx.x;
+    const long long n2 = (long long)side * side;
+    const long long o = i * n2;
+    if (threadIdx.x == 0) {
+        box[i] = make_int4(0, 0, side, side);
+        off[i] = o;
+    }
+    const double m = mass[i];
+    for (long long k = threadIdx.x; k < n2; k += blockDim.x) pool[o + k] = m * nu[k];
+}
+
+// ------------------------------------------------------------------- K2 --
+// Exclusive scan of the (16-byte padded) box areas in basic-cell order:
+// deterministic pool layout.  Single block of 1024 threads.
+__global__ void k_scan_areas(const int4* __restrict__ box, long long* __restrict__ newoff,
+                             long long* __restrict__ total, int n, long long* __restrict__ entries) {
+    __shared__ long long part[1024];
+    __shared__ long long epart[1024];
+    const int t = threadIdx.x;
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int b = t * per, e = min(n, b + per);
+    long long s = 0, se = 0;
+    for (int k = b; k < e; ++k) {
+        const long long a = (long long)box[k].z * box[k].w;
+        s += (a + 1) & ~1LL;
+        se += a;
+    }
+    part[t] = s;
+    epart[t] = se;
+    __syncthreads();
+    if (t == 0) {
+        long long acc = 0, acce = 0;
+        for (int k = 0; k < (int)blockDim.x; ++k) {
+            const long long v = part[k];
+            part[k] = acc;
+            acc += v;
+            acce += epart[k];
+        }
+        *total = acc;
+        if (entries) *entries = acce;
+    }
+    __syncthreads();
+    long long o = part[t];
+    for (int k = b; k < e; ++k) {
+        newoff[k] = o;
+        const long long a = (long long)box[k].z * box[k].w;
+        o += (a + 1) & ~1LL;
+    }
+}
+
+// Copy every box from the scratch layout into the ordered pool (one warp per box).
+__global__ void k_copy_boxes(const int4* __restrict__ box, const long long* __restrict__ srcoff,
+                             const long long* __restrict__ dstoff, const double* __restrict__ src,
+                             double* __restrict__ dst, int n, long long cap) {
+    const int warps = blockDim.x >> 5;
+    const int w = blockIdx.x * warps + (threadIdx.x >> 5);
+    const int l = threadIdx.x & 31;
+    if (w >= n) return;
+    const long long a = (long long)box[w].z * box[w].w;
+    const long long so = srcoff[w], d0 = dstoff[w];
+    if (d0 + a > cap) return;
+    const double2* s2 = reinterpret_cast<const double2*>(src + so);
+    double2* d2 = reinterpret_cast<double2*>(dst + d0);
+    const long long a2 = a >> 1;
+    for (long long k = l; k < a2; k += 32) d2[k] = s2[k];
+    if ((a & 1) && l == 0) dst[d0 + a - 1] = src[so + a - 1];
+}
+
+// ------------------------------------------------------------------- K3 --
+// Fixed-order reduction of the per-cell outputs into the sweep statistics
+// (one block of 1024 threads; thread t owns cells t, t+1024, ... in order).
+__global__ void k_reduce_stats(const CellOut* __restrict__ out, int ncells, DevStats* last, DevStats* tot,
+                               const long long* __restrict__ entries, const int* __restrict__ n_deferred,
+                               const int* __restrict__ overflow) {
+    __shared__ double s_err[1024], s_mufu[1024];
+    __shared__ long long s_it[1024], s_fb[1024];
+    __shared__ int s_max[1024], s_fail[1024], s_box[1024];
+    const int t = threadIdx.x;
+    double er = 0.0, mf = 0.0;
+    long long it = 0, fb = 0;
+    int mx = 0, fl = 0, bx = 0;
+    for (int c = t; c < ncells; c += blockDim.x) {
+        const CellOut o = out[c];
+        er += (double)o.err;
+        mf += o.mufu;
+        it += o.iters;
+        fb += o.fallbacks;
+        mx = max(mx, o.iters);
+        fl += (o.flags & 3) ? 1 : 0;
+        bx = max(bx, o.box);
+    }
+    s_err[t] = er; s_mufu[t] = mf; s_it[t] = it; s_fb[t] = fb; s_max[t] = mx; s_fail[t] = fl; s_box[t] = bx;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (t < w) {
+            s_err[t] += s_err[t + w];
+            s_mufu[t] += s_mufu[t + w];
+            s_it[t] += s_it[t + w];
+            s_fb[t] += s_fb[t + w];
+            s_max[t] = max(s_max[t], s_max[t + w]);
+            s_fail[t] += s_fail[t + w];
+            s_box[t] = max(s_box[t], s_box[t + w]);
+        }
+        __syncthreads();
+    }
+    if (t == 0) {
+        DevStats L;
+        L.cells = ncells;
+        L.iters_sum = s_it[0];
+        L.iters_max = s_max[0];
+        L.failed = s_fail[0];
+        L.err_sum = s_err[0];
+        L.mufu = s_mufu[0];
+        L.fallbacks = s_fb[0];
+        L.deferred = *n_deferred;
+        L.max_box = s_box[0];
+        L.overflow = *overflow;
+        L.entries = *entries;
+        *last = L;
+        tot->cells += L.cells;
+        tot->iters_sum += L.iters_sum;
+        tot->iters_max = max(tot->iters_max, L.iters_max);
+        tot->failed += L.failed;
+        tot->err_sum += L.err_sum;
+        tot->mufu += L.mufu;
+        tot->fallbacks += L.fallbacks;
+        tot->deferred += L.deferred;
+        tot->max_box = max(tot->max_box, L.max_box);
+        tot->overflow |= L.overflow;
+        tot->entries = L.entries;
+    }
+}
+
+// ------------------------------------------------------------------- K4 --
+// Fine boxes = 2x the parent box (Pa(i) = coarse cell containing X_i).
+__global__ void k_refine_boxes(const int4* __restrict__ cbox, int4* __restrict__ fbox, int nbc, int nbf) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nbf * nbf) return;
+    const int ir = i / nbf, ic = i % nbf;
+    const int j = (ir * nbc / nbf) * nbc + (ic * nbc / nbf);
+    const int4 b = cbox[j];
+    fbox[i] = make_int4(2 * b.x, 2 * b.y, 2 * b.z, 2 * b.w);
+}
+
+// nu_i^0(y) = nu(y) nuhat_{Pa(i)}(pa(y)) / nuhat(pa(y)) * mu(X_i) / muhat(Xhat_{Pa(i)}), 0/0 := 0.
+__global__ void k_refine_fill(const int4* __restrict__ cbox, const long long* __restrict__ coff,
+                              const double* __restrict__ cpool, const int4* __restrict__ fbox,
+                              const long long* __restrict__ foff, double* __restrict__ fpool,
+                              const double* __restrict__ cnu, const double* __restrict__ fnu,
+                              const double* __restrict__ cmass, const double* __restrict__ fmass,
+                              int nbc, int nbf, int sidec, int sidef, long long cap, int* overflow) {
+    const int i = blockIdx.x;
+    const int ir = i / nbf, ic = i % nbf;
+    const int j = (ir * nbc / nbf) * nbc + (ic * nbc / nbf);
+    const int4 pb = cbox[j];
+    const int4 fb = fbox[i];
+    const long long area = (long long)fb.z * fb.w;
+    const long long o = foff[i];
+    if (o + area > cap) {
+        if (threadIdx.x == 0) atomicOr(overflow, 1);
+        return;
+    }
+    const double ratio = fmass[i] / cmass[j];
+    const long long co = coff[j];
+    for (long long k = threadIdx.x; k < area; k += blockDim.x) {
+        const int y1 = fb.x + (int)(k / fb.w), y2 = fb.y + (int)(k % fb.w);
+        const int p1 = y1 >> 1, p2 = y2 >> 1;
+        const double nhj = cpool[co + (long long)(p1 - pb.x) * pb.w + (p2 - pb.y)];
+        const double nh = cnu[(long long)p1 * sidec + p2];
+        const double nv = fnu[(long long)y1 * sidef + y2];
+        fpool[o + k] = (nh > 0.0) ? nv * (nhj / nh) * ratio : 0.0;
+    }
+}
+
+// ------------------------------------------------------------------- K6 --
+// sum_i nu_i(y) as 2^60 fixed point (deterministic atomics), one block per box.
+__global__ void k_scatter_y(const int4* __restrict__ box, const long long* __restrict__ off,
+                            const double* __restrict__ pool, unsigned long long* acc, int side) {
+    const int i = blockIdx.x;
+    const int4 b = box[i];
+    const long long o = off[i];
+    const long long area = (long long)b.z * b.w;
+    for (long long k = threadIdx.x; k < area; k += blockDim.x) {
+        const double v = pool[o + k];
+        if (v != 0.0) {
+            const long long y = (long long)(b.x + k / b.w) * side + (b.y + k % b.w);
+            atomicAdd(&acc[y], (unsigned long long)llrint(v * 1152921504606846976.0));
+        }
+    }
+}
+
+__global__ void k_l1_y(const unsigned long long* __restrict__ acc, const double* __restrict__ nu, long long n,
+                       double* __restrict__ partial) {
+    __shared__ double red[32];
+    double s = 0.0;
+    const long long per = (n + gridDim.x - 1) / gridDim.x;
+    const long long b = blockIdx.x * per, e = min(n, b + per);
+    for (long long k = b + threadIdx.x; k < e; k += blockDim.x)
+        s += fabs((double)acc[k] * (1.0 / 1152921504606846976.0) - nu[k]);
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// Fixed-order sum of n doubles (single block).
+__global__ void k_sum(const double* __restrict__ x, int n, int stride, double* out) {
+    __shared__ double red[32];
+    double s = 0.0;
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int b = threadIdx.x * per, e = min(n, b + per);
+    for (int k = b; k < e; ++k) s += x[(long long)k * stride];
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) *out = s;
+}
+
+// ------------------------------------------------------------------- K7 --
+// fp64 dense evaluation of the plan of each cell of partition `part`:
+// f = alpha + eps log mu, g from one Y-iteration on nu_cell = sum_{i in J} nu_i,
+// pi = exp((f + g - c)/eps).  Outputs per cell: <c,pi>, eps(KL - ||K||) part,
+// sum_x |P_X pi - mu|.  Optional COO export.  Global scratch per block.
+__global__ void k_eval_cells(EvalParams p) {
+    __shared__ double red[32];
+    __shared__ int4 s_box[4];
+    __shared__ long long s_off[4];
+    const int cell = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int cp = cell / p.nca, cq = cell % p.nca;
+    int rlo, rhi, clo, chi;
+    cell_span(p.nb, p.part, cp, rlo, rhi);
+    cell_span(p.nb, p.part, cq, clo, chi);
+    const int ncol = chi - clo + 1, nmem = (rhi - rlo + 1) * ncol;
+    if (tid < nmem) {
+        const int i = (rlo + tid / ncol) * p.nb + clo + tid % ncol;
+        s_box[tid] = p.box[i];
+        s_off[tid] = p.off[i];
+    }
+    __syncthreads();
+    const int ar = (rhi - rlo + 1) * p.s, ac = ncol * p.s;
+    const int R0 = rlo * p.s, C0 = clo * p.s;
+    int y0 = 1 << 30, x0 = 1 << 30, y1 = -1, x1 = -1;
+    for (int m = 0; m < nmem; ++m) {
+        const int4 b = s_box[m];
+        if (b.z <= 0 || b.w <= 0) continue;
+        y0 = min(y0, b.x); x0 = min(x0, b.y);
+        y1 = max(y1, b.x + b.z - 1); x1 = max(x1, b.y + b.w - 1);
+    }
+    const int br = y1 >= 0 ? y1 - y0 + 1 : 0, bc = x1 >= 0 ? x1 - x0 + 1 : 0;
+    const int nx = ar * ac, ny = br * bc;
+    double* nuc = p.scratch + (long long)cell * p.scratch_per_cell;
+    double* g = nuc + p.max_ny;
+    double* f = g + p.max_ny;
+    const double h = 1.0 / p.side;
+    const double eps = p.eps;
+    for (int y = tid; y < ny; y += blockDim.x) {
+        const int gy = y0 + y / bc, gx = x0 + y % bc;
+        double v = 0.0;
+        for (int m = 0; m < nmem; ++m) {
+            const int4 b = s_box[m];
+            const int ry = gy - b.x, rx = gx - b.y;
+            if (ry >= 0 && ry < b.z && rx >= 0 && rx < b.w) v += p.pool[s_off[m] + (long long)ry * b.w + rx];
+        }
+        nuc[y] = v;
+    }
+    for (int x = tid; x < nx; x += blockDim.x) {
+        const long long gi = (long long)(R0 + x / ac) * p.side + (C0 + x % ac);
+        f[x] = p.mu[gi] > 0.0 ? p.alpha[gi] + eps * p.logmu[gi] : -INFINITY;
+    }
+    __syncthreads();
+    // Y-iteration (Remark Sinkhorn P:272): g(y) = eps log nu_cell(y) - eps LSE_x[(f - c)/eps]
+    for (int y = tid; y < ny; y += blockDim.x) {
+        if (!(nuc[y] > 0.0)) { g[y] = -INFINITY; continue; }
+        const double yy1 = (y0 + y / bc + 0.5) * h, yy2 = (x0 + y % bc + 0.5) * h;
+        double m = -INFINITY;
+        for (int x = 0; x < nx; ++x) {
+            const double d1 = (R0 + x / ac + 0.5) * h - yy1, d2 = (C0 + x % ac + 0.5) * h - yy2;
+            m = fmax(m, f[x] - (d1 * d1 + d2 * d2));
+        }
+        double s = 0.0;
+        for (int x = 0; x < nx; ++x) {
+            const double d1 = (R0 + x / ac + 0.5) * h - yy1, d2 = (C0 + x % ac + 0.5) * h - yy2;
+            s += exp((f[x] - (d1 * d1 + d2 * d2) - m) / eps);
+        }
+        g[y] = eps * log(nuc[y]) - (m + eps * log(s));
+    }
+    __syncthreads();
+    double cost = 0.0, ent = 0.0, l1x = 0.0;
+    for (int x = tid; x < nx; x += blockDim.x) {
+        const long long gi = (long long)(R0 + x / ac) * p.side + (C0 + x % ac);
+        const double xx1 = (R0 + x / ac + 0.5) * h, xx2 = (C0 + x % ac + 0.5) * h;
+        double px = 0.0;
+        if (f[x] > -INFINITY) {
+            const double elm = eps * p.logmu[gi];
+            for (int y = 0; y < ny; ++y) {
+                if (g[y] == -INFINITY) {
+                    if (p.coo) {
+                        const long long k = p.coo_off[cell] + (long long)x * ny + y;
+                        p.coo_x[k] = (int)gi; p.coo_y[k] = 0; p.coo_m[k] = 0.0;
+                    }
+                    continue;
+                }
+                const int gy = y0 + y / bc, gx = x0 + y % bc;
+                const double d1 = xx1 - (gy + 0.5) * h, d2 = xx2 - (gx + 0.5) * h;
+                const double c = d1 * d1 + d2 * d2;
+                const double pi = exp((f[x] + g[y] - c) / eps);
+                const long long gyi = (long long)gy * p.side + gx;
+                px += pi;
+                cost += c * pi;
+                ent += pi * (f[x] + g[y] - elm - eps * log(p.nu[gyi]) - eps);
+                if (p.coo) {
+                    const long long k = p.coo_off[cell] + (long long)x * ny + y;
+                    p.coo_x[k] = (int)gi; p.coo_y[k] = (int)gyi; p.coo_m[k] = pi;
+                }
+            }
+        } else if (p.coo) {
+            for (int y = 0; y < ny; ++y) {
+                const long long k = p.coo_off[cell] + (long long)x * ny + y;
+                p.coo_x[k] = (int)gi; p.coo_y[k] = 0; p.coo_m[k] = 0.0;
+            }
+        }
+        l1x += fabs(px - p.mu[gi]);
+    }
+    cost = block_sum(cost, red);
+    ent = block_sum(ent, red);
+    l1x = block_sum(l1x, red);
+    if (tid == 0) {
+        p.cell_res[3 * cell + 0] = cost;
+        p.cell_res[3 * cell + 1] = ent;
+        p.cell_res[3 * cell + 2] = l1x;
+    }
+}
+
+// ------------------------------------------------------- MUFU roofline --
+// 8 independent ex2 chains per thread; x <- 2^(-x) stays in (0, 1].
+__global__ void k_mufu_bench(float* out, int iters) {
+    float a0 = threadIdx.x * 1e-3f, a1 = a0 + 0.1f, a2 = a0 + 0.2f, a3 = a0 + 0.3f;
+    float a4 = a0 + 0.4f, a5 = a0 + 0.5f, a6 = a0 + 0.6f, a7 = a0 + 0.7f;
+    for (int i = 0; i < iters; ++i) {
+        a0 = ex2f(-a0); a1 = ex2f(-a1); a2 = ex2f(-a2); a3 = ex2f(-a3);
+        a4 = ex2f(-a4); a5 = ex2f(-a5); a6 = ex2f(-a6); a7 = ex2f(-a7);
+    }
+    const float s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (s == 12345.0f) out[blockIdx.x] = s;   // never true; keeps the chains alive
+}
+
+// --------------------------------------------------------- host wrappers --
+#define LAUNCH_CHECK() do { cudaError_t _e = cudaGetLastError(); if (_e != cudaSuccess) return _e; } while (0)
+
+static int grid_for(long long n, int threads) {
+    long long g = (n + threads - 1) / threads;
+    if (g > 148 * 32) g = 148 * 32;
+    return (int)(g < 1 ? 1 : g);
+}
+
+cudaError_t launch_pool2x2(const double* fine, double* coarse, int sc, cudaStream_t st) {
+    k_pool2x2<<<grid_for((long long)sc * sc, 256), 256, 0, st>>>(fine, coarse, sc);
+    LAUNCH_CHECK(); return cudaSuccess;
+}
+cudaError_t launch_log(const double* x, double* lx, long long n, cudaStream_t st) {
+    k_log<<<grid_for(n, 256), 256, 0, st>>>(x, lx, n);
+    LAUNCH_CHECK(); return cudaSuccess;
+}
+cudaError_t launch_mass_i(const double* mu, double* mass, int side, int s, int nb, cudaStream_t st) {
+    k_mass_i<<<nb * nb, 256, 0, st>>>(mu, mass, side, s, nb);
+    LAUNCH_CHECK(); return cudaSuccess;
+}
+cudaError_t launch_product_init(int4* box, long long* off, double* pool, const double* mass, const double* nu,
+                                int side, int nb, cudaStream_t st) {
+    k_product_init<<<nb * nb, 256, 0, st>>>(box, off, pool, mass, nu, side);
+    LAUNCH_CHECK(); return cudaSuccess;
+}
+cudaError_t launch_scan_areas(const int4* box, long long* newoff, long long* total, int n, long long* entries,
+                              cudaStream_t st) {
+    k_scan_areas<<<1, 1024, 0, st>>>(box, newoff, total, n, entries);
+    LAUNCH_CHECK(); return cudaSuccess;
+}
+cudaError_t launch_copy_boxes(const int4* box, const long long* srcoff, const long long* dstoff, const double* src,
+                              double* dst, int n, long long cap, cudaStream_t st) {
+    const int wpb = 8;
+    k_copy_boxes<<<(n + wpb - 1) / wpb, 32 * wpb, 0, st>>>(box, srcoff, dstoff, src, dst, n, cap);
+    LAUNCH_CHECK(); return cudaSuccess;
+}
+cudaError_t launch_reduce_stats(const CellOut* out, int ncells, DevStats* last, DevStats* tot,
+                                const long long* entries, const int* n_deferred, const int* overflow,
+                                cudaStream_t st) {
+    k_reduce_stats<<<1, 1024, 0, st>>>(out, ncells, last, tot, entries, n_deferred, overflow);
+    LAUNCH_CHECK(); return cudaSuccess;
+}
+cudaError_t launch_refine(const int4* cbox, const long long* coff, const double* cpool, int4* fbox,
+                          long long* foff, double* fpool, const double* cnu, const double* fnu,
+                          const double* cmass, const double* fmass, int nbc, int nbf, int sidec, int sidef,
+                          long long cap, int* overflow, long long* total, long long* entries, cudaStream_t st) {
+    k_refine_boxes<<<(nbf * nbf + 255) / 256, 256, 0, st>>>(cbox, fbox, nbc, nbf);
+    LAUNCH_CHECK();
+    k_scan_areas<<<1, 1024, 0, st>>>(fbox, foff, total, nbf * nbf, entries);
+    LAUNCH_CHECK();
+    k_refine_fill<<<nbf * nbf, 256, 0, st>>>(cbox, coff, cpool, fbox, foff, fpool, cnu, fnu, cmass, fmass,
+                                             nbc, nbf, sidec, sidef, cap, overflow);
+    LAUNCH_CHECK(); return cudaSuccess;
+}
+cudaError_t launch_scatter_l1y(const int4* box, const long long* off, const double* pool, int nb,
+                               unsigned long long* acc, const double* nu, int side, double* partial,
+                               double* out, cudaStream_t st) {
+    const long long n2 = (long long)side * side;
+    cudaError_t e = cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * n2, st);
+    if (e != cudaSuccess) return e;
+    k_scatter_y<<<nb * nb, 256, 0, st>>>(box, off, pool, acc, side);
+    LAUNCH_CHECK();
+    const int nblk = 256;
+    k_l1_y<<<nblk, 256, 0, st>>>(acc, nu, n2, partial);
+    LAUNCH_CHECK();
+    k_sum<<<1, 256, 0, st>>>(partial, nblk, 1, out);
+    LAUNCH_CHECK(); return cudaSuccess;
+}
+cudaError_t launch_eval(const EvalParams& p, int ncells, double* sums, cudaStream_t st) {
+    k_eval_cells<<<ncells, 256, 0, st>>>(p);
+    LAUNCH_CHECK();
+    for (int k = 0; k < 3; ++k) {
+        k_sum<<<1, 256, 0, st>>>(p.cell_res + k, ncells, 3, sums + k);
+        LAUNCH_CHECK();
+    }
+    return cudaSuccess;
+}
+cudaError_t launch_mufu_bench(float* out, int blocks, int threads, int iters, cudaStream_t st) {
+    k_mufu_bench<<<blocks, threads, 0, st>>>(out, iters);
+    LAUNCH_CHECK(); return cudaSuccess;
+}
+
+}  // namespace dd

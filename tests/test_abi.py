@@ -1,0 +1,82 @@
+"""CPU-side checks of the boundary: the C-ABI library builds for sm_100a, loads
+without a GPU, and exports every symbol include/dd.h declares (no compute
+calls).  The product package never imports the oracle."""
+import ast
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_symbols():
+    src = open(os.path.join(ROOT, "include", "dd.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(dd_[a-z_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def gpu_lib():
+    from paper_2001_10986_b200 import build as b
+    b.build()
+    from paper_2001_10986_b200 import lib
+    return lib()
+
+
+def test_header_symbols_exported(gpu_lib):
+    syms = _header_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(gpu_lib, s), f"{s} declared in dd.h but not exported"
+
+
+def test_binding_lists_every_symbol():
+    from paper_2001_10986_b200.dd import EXPORTS
+    assert sorted(EXPORTS) == _header_symbols()
+
+
+def test_version_and_schedule_without_gpu(gpu_lib):
+    from paper_2001_10986_b200 import build_schedule
+    assert gpu_lib.dd_version().decode().startswith("ddot-b200")
+    # host-only entry point: the driver's schedule, same counts as the paper
+    assert sum(w for _, _, w in build_schedule(256, 8, 0.25)) == 50
+    assert sum(w for _, _, w in build_schedule(2048, 8, 0.5)) == 72
+
+
+def test_no_cpu_fallback_without_gpu(gpu_lib):
+    """Without an sm_100 device dd_init must fail loudly (DD_ECUDA)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import numpy as np
+    from paper_2001_10986_b200 import DD
+    mu = np.full((16, 16), 1 / 256)
+    with pytest.raises(RuntimeError, match="rc=4"):
+        DD(mu, mu, 2 / 256, 4)
+
+
+def test_sm100a_code_in_library(gpu_lib):
+    """The fatbinary holds sm_100a SASS (cuobjdump) with MUFU.EX2 and packed FP32x2 ops."""
+    import subprocess
+    from paper_2001_10986_b200 import SO_PATH
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", SO_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert "MUFU.EX2" in out
+    assert "FFMA2" in out and "FADD2" in out
+
+
+def test_product_package_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2001_10986_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                tree = ast.parse(open(os.path.join(dirpath, f)).read())
+                for node in ast.walk(tree):
+                    if isinstance(node, ast.Import):
+                        assert all(not a.name.startswith("oracle") for a in node.names)
+                    if isinstance(node, ast.ImportFrom):
+                        assert not (node.module or "").startswith("oracle")
+            if f.endswith((".cu", ".cuh", ".h", ".cpp")):
+                assert "dd_oracle" not in open(os.path.join(dirpath, f)).read()

@@ -1,0 +1,171 @@
+"""GPU (B200) parity: the CUDA path through the C-ABI vs the fp64 CPU oracle on
+the same seeded inputs.  Gates (BASELINE.json north_star):
+relative primal transport cost <= 1e-5, GPU marginal L1 errors <= 1e-6.
+
+Tolerances derived in DESIGN.md "Parity tolerances": per composite cell the
+GPU's fp32 Sinkhorn floors at ~1e-7 relative in the plan, the oracle's fp64 at
+~1e-14; both stop at Err = 1e-6 in the L1 X-error, so two correct solves of
+the same cell problem differ by at most ~2 Err ||mu_J|| in L1."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from ddinputs import config_images, gaussian_mixture_image, product_image  # noqa: E402
+from oracle import Oracle  # noqa: E402
+from oracle.oracle import SCHED_LADDER as O_LADDER  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def DD():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2001_10986_b200 import DD as _DD
+    return _DD
+
+
+def _mass_i(mu, s):
+    n = mu.shape[0]
+    nb = n // s
+    return mu.reshape(nb, s, nb, s).sum((1, 3)).ravel()
+
+
+def test_device_and_library(DD):
+    import torch
+    from paper_2001_10986_b200 import lib
+    assert torch.cuda.get_device_capability(0)[0] == 10
+    assert lib().dd_version().decode().startswith("ddot-b200")
+
+
+def test_single_sweep_parity_from_product_state(DD):
+    """Same input state (product coupling) -> one A-sweep and one B-sweep on both;
+    compare every basic-cell marginal nu_i (the paper's state)."""
+    mu, nu = config_images(1)
+    eps = 2.0 / 32**2
+    g = DD(mu, nu, eps, 4, err_tol=1e-6)
+    o = Oracle(mu, nu, eps, 4, err_tol=1e-6)
+    mass = _mass_i(mu, 4)
+    for sweep in range(2):
+        g.iterate(1)
+        o.iterate(1)
+        Dg = g.basic_marginals_dense()
+        Do = o.basic_marginals_dense()
+        diff = np.abs(Dg - Do).sum(1)
+        # per basic cell: |nu_i^gpu - nu_i^ora|_1 <= 2 Err ||mu_J|| (both within Err of the cell optimum)
+        assert (diff <= 4e-6 * np.maximum(mass, 1e-3)).all(), (sweep, diff.max())
+        assert np.abs(Dg - Do).sum() <= 4e-6
+        # the paper's invariants on the GPU state
+        assert np.abs(Dg.sum(0) - nu.ravel()).sum() < 1e-11
+        np.testing.assert_allclose(Dg.sum(1), mass, rtol=1e-10, atol=1e-12)
+    sg, so = g.stats(), o.stats()
+    assert sg["cells"] == so["cells"] == 25
+    assert sg["err_x_sum"] <= 1e-6 * 1.0001
+
+
+def test_trajectory_parity_cfg1(DD):
+    """Config 1 (32^2, s = 4, kappa = 2 fixed): 16 sweeps on both."""
+    mu, nu = config_images(1)
+    eps = 2.0 / 32**2
+    g = DD(mu, nu, eps, 4, err_tol=1e-6)
+    o = Oracle(mu, nu, eps, 4, err_tol=1e-6)
+    g.iterate(16)
+    o.iterate(16)
+    cg, eg = g.primal_cost()
+    co, eo = o.primal_cost()
+    assert abs(cg - co) <= 1e-5 * co
+    assert abs(eg - eo) <= 1e-5 * abs(eo)
+    lx, ly = g.marginal_error()
+    assert lx <= 1e-6 and ly <= 1e-6
+    lxo, _ = o.marginal_error()
+    st = g.totals()
+    sto = o.stats()
+    assert st["cells"] == 8 * 16 + 8 * 25
+    # iteration counts agree within a few percent (stop tests in fp32 vs fp64)
+    assert abs(g.stats()["iters_sum"] - sto["iters_sum"]) <= 0.1 * sto["iters_sum"] + 20
+
+
+def test_plan_parity_small(DD):
+    """COO plans of the last sweep agree entrywise (L1) on a 16^2 problem."""
+    mu, nu = gaussian_mixture_image(16, 3, 1), gaussian_mixture_image(16, 4, 1)
+    eps = 2.0 / 16**2
+    g = DD(mu, nu, eps, 4, err_tol=1e-7)
+    o = Oracle(mu, nu, eps, 4, err_tol=1e-7)
+    g.iterate(8)
+    o.iterate(8)
+    Pg, Po = g.plan_dense(), o.plan_dense()
+    assert np.abs(Pg - Po).sum() <= 1e-6
+    assert np.abs(Pg.sum(0) - nu.ravel()).sum() <= 1e-6
+    assert np.abs(Pg.sum(1) - mu.ravel()).sum() <= 1e-6
+
+
+def test_ladder_parity_cfg2(DD):
+    """Config 2: 64^2, coarse-to-fine from 16^2 with eps from 1.0 to 0.5 h^2."""
+    mu, nu = config_images(2)
+    eps = 0.5 / 64**2
+    kw = dict(err_tol=1e-6, eps_start=1.0, coarsest_side=16)
+    g = DD(mu, nu, eps, 4, schedule=1, **kw)
+    o = Oracle(mu, nu, eps, 4, schedule=O_LADDER, **kw)
+    g.run_schedule()
+    o.run_schedule()
+    cg, _ = g.primal_cost()
+    co, _ = o.primal_cost()
+    assert abs(cg - co) <= 1e-5 * co, (cg, co)
+    lx, ly = g.marginal_error()
+    assert lx <= 1e-6 and ly <= 1e-6, (lx, ly)
+    assert g.state_info()["half_index"] == o.state_info()["half_index"] == 38
+
+
+@pytest.mark.parametrize("n,s,kappa", [(8, 4, 2.0), (16, 4, 0.5), (16, 8, 1.0), (64, 8, 2.0)])
+def test_edge_geometries(DD, n, s, kappa):
+    """Degenerate partitions: one A-cell (n = 2s), B corner singletons,
+    2x1 edge cells, s = 8 composite cells; both sweeps, several sweeps."""
+    mu, nu = gaussian_mixture_image(n, 5, 1), gaussian_mixture_image(n, 6, 1)
+    eps = kappa / n**2
+    g = DD(mu, nu, eps, s)
+    o = Oracle(mu, nu, eps, s)
+    g.iterate(4)
+    o.iterate(4)
+    cg, _ = g.primal_cost()
+    co, _ = o.primal_cost()
+    assert abs(cg - co) <= 1e-5 * co
+    lx, ly = g.marginal_error()
+    assert lx <= 1e-6 and ly <= 1e-6
+
+
+def test_no_truncation_exact_mode(DD):
+    """tau = 0 and tight Err: GPU reaches its fp32 floor, still <= 1e-6 from the oracle."""
+    mu, nu = gaussian_mixture_image(16, 7, 1), gaussian_mixture_image(16, 8, 1)
+    eps = 2.0 / 16**2
+    g = DD(mu, nu, eps, 4, err_tol=1e-7, no_truncate=True)
+    o = Oracle(mu, nu, eps, 4, err_tol=1e-7, no_truncate=True)
+    g.iterate(10)
+    o.iterate(10)
+    Dg, Do = g.basic_marginals_dense(), o.basic_marginals_dense()
+    assert np.abs(Dg - Do).sum() <= 1e-6
+
+
+def test_set_state_roundtrip(DD):
+    """The oracle's exported state imported into the GPU library gives the same
+    next sweep (state import path of DESIGN.md single-sweep parity)."""
+    mu, nu = config_images(1)
+    eps = 2.0 / 32**2
+    o = Oracle(mu, nu, eps, 4)
+    o.iterate(3)
+    st = o.get_state()
+    g = DD(mu, nu, eps, 4)
+    g.set_state(st)
+    back = g.get_state()
+    assert np.array_equal(back["boxes"], st["boxes"])
+    assert np.array_equal(back["values"], st["values"])
+    g.iterate(1)
+    o.iterate(1)
+    assert np.abs(g.basic_marginals_dense() - o.basic_marginals_dense()).sum() <= 4e-6
+
+
+def test_validation_errors_gpu(DD):
+    mu = np.full((16, 16), 1 / 256)
+    with pytest.raises(ValueError):
+        DD(mu, mu * 1.01, 1.0, 4)
+    with pytest.raises(ValueError):
+        DD(mu, mu, 1.0, 16)

@@ -8,7 +8,7 @@ struct DevStats {
     long long cells, iters_sum;
     int iters_max, failed;
     double err_sum, mufu;
-    long long fallbacks, deferred;
+    long long fallbacks, deferred, huge;
     int max_box, overflow;
     long long entries;
 };
@@ -35,7 +35,8 @@ struct EvalParams {
 };
 
 size_t k1_smem_bytes_host(int s, int bcap);
-cudaError_t launch_k1(const SweepParams& p, int grid, size_t smem, cudaStream_t st);
+cudaError_t launch_k1(const SweepParams& p, int tier, int grid, size_t smem, cudaStream_t st);
+cudaError_t launch_k0(const SweepParams& p, int b0, int b1, int* lists, int* counts, int ncap, cudaStream_t st);
 cudaError_t launch_pool2x2(const double* fine, double* coarse, int sc, cudaStream_t st);
 cudaError_t launch_log(const double* x, double* lx, long long n, cudaStream_t st);
 cudaError_t launch_mass_i(const double* mu, double* mass, int side, int s, int nb, cudaStream_t st);
@@ -47,7 +48,7 @@ cudaError_t launch_copy_boxes(const int4* box, const long long* srcoff, const lo
                               double* dst, int n, long long cap, cudaStream_t st);
 cudaError_t launch_reduce_stats(const CellOut* out, int ncells, DevStats* last, DevStats* tot,
                                 const long long* entries, const int* n_deferred, const int* overflow,
-                                cudaStream_t st);
+                                const int* n_huge, cudaStream_t st);
 cudaError_t launch_refine(const int4* cbox, const long long* coff, const double* cpool, int4* fbox,
                           long long* foff, double* fpool, const double* cnu, const double* fnu,
                           const double* cmass, const double* fmass, int nbc, int nbf, int sidec, int sidef,

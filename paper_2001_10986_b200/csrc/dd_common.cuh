@@ -38,7 +38,9 @@ struct SweepParams {
     double err_tol;       // Err
     int max_iter;
     int bcap;             // max Y-box side this launch handles
-    int mode;             // 0: one CTA per cell (defer big ones); 1: work list
+    int mode;             // 0: one CTA per cell; 1: work list in SMEM; 2: work list in global scratch
+    unsigned char* gscratch;    // mode 2: per-CTA slice of global memory replacing SMEM
+    long long gslice;           // bytes per CTA slice
     int4* box;            // nb*nb (y0r, y0c, hr, hc), updated in place
     long long* off;       // nb*nb offsets (in: pool_in, out: scratch)
     const double* pool_in;
@@ -50,9 +52,11 @@ struct SweepParams {
     const double* logmu;  // layer log mu (-inf where 0)
     const double* mass_i; // nb*nb
     CellOut* out;         // ncells
-    int* deferred;        // list of deferred cell ids
-    int* n_deferred;
-    int* work_counter;    // mode 1 dynamic work index
+    int* list_in;         // modes 1/2: cells to solve
+    int* n_in;
+    int* list_out;        // modes 0/1: cells whose Y box exceeds bcap (next tier)
+    int* n_out;
+    int* work_counter;    // modes 1/2 dynamic work index
     int* overflow;        // set if scratch capacity exceeded
 };
 

@@ -55,8 +55,13 @@ struct dd_ctx {
     long long cap = 0;
     // sweep plumbing
     unsigned long long* bump = nullptr;
-    int* deferred = nullptr;
-    int* counters = nullptr;        // [0] n_deferred, [1] work_counter, [2] overflow
+    int* lists = nullptr;           // tier lists [3][ncell_max] (K0)
+    int* counters = nullptr;        // [0..2] tier counts, [3..5] work counters, [6] overflow
+    unsigned char* huge = nullptr;  // global-memory slices of the tier-2 (largest box) path
+    long long huge_slice = 0;
+    int grid_huge = 0, bcap_huge = 512;
+    cudaStream_t st_t[2] = {nullptr, nullptr};   // tier 1 / tier 2 streams
+    cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
     CellOut* cellout = nullptr;
     long long* d_total = nullptr;   // [0] padded pool length, [1] entries
     DevStats* d_last = nullptr;
@@ -164,34 +169,38 @@ int harvest(dd_ctx* c) {
 
 int check_overflow(dd_ctx* c) {
     int ov = 0;
-    CK(cudaMemcpyAsync(&ov, c->counters + 2, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(&ov, c->counters + 6, sizeof(int), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     if (ov & 1) {
         set_err(c, "nu_i pool capacity (%lld entries) exceeded; raise dd_options.pool_capacity", c->cap);
         return DD_ENOMEM;
     }
     if (ov & 2) {
-        set_err(c, "a composite cell's Y box exceeds the largest supported box side (%d)", c->bcap_big);
+        set_err(c, "a composite cell's Y box exceeds the largest supported box side (%d)", c->bcap_huge);
         return DD_ENOMEM;
     }
     return DD_OK;
 }
 
 void choose_caps(dd_ctx* c, int s) {
-    // main launch: SMEM for boxes up to bcap_main; larger cells go to the big path
-    int want = (s <= 4) ? 24 : 32;
+    // tier 0: SMEM for union Y boxes <= bcap_main (several CTAs per SM);
+    // tier 1: one CTA per SM with up to ~220 KB SMEM; tier 2: global slices
+    int want = (s <= 4) ? 32 : 40;
     if (c->opt.reserved[0] > 0) want = c->opt.reserved[0];
     if (want < 2 * s + 2) want = 2 * s + 2;
     c->bcap_main = want;
     c->smem_main = k1_smem_bytes_host(s, want);
     int big = want;
-    while (k1_smem_bytes_host(s, big + 1) <= 220 * 1024) ++big;
+    while (k1_smem_bytes_host(s, big + 1) <= 216 * 1024) ++big;
     c->bcap_big = big;
     c->smem_big = k1_smem_bytes_host(s, big);
 }
 
 // One sweep (Alg. 2 lines 6-14) over the partition selected by the parity of
 // the half-iteration index (line 7: odd l -> A).
+//   K0 classify cells by union Y-box side -> tier lists
+//   tiers 2 | 1 | 0 run concurrently on three streams (fork/join events)
+//   K2 deterministic compaction, K3 fixed-order statistics
 int sweep(dd_ctx* c) {
     Layer& Lr = c->L[c->cur];
     const int part = (c->half_index % 2 == 0) ? 1 : 2;
@@ -199,7 +208,7 @@ int sweep(dd_ctx* c) {
     const int ncells = nca * nca;
     choose_caps(c, Lr.s);
     CK(cudaMemsetAsync(c->bump, 0, sizeof(unsigned long long), c->st));
-    CK(cudaMemsetAsync(c->counters, 0, 2 * sizeof(int), c->st));
+    CK(cudaMemsetAsync(c->counters, 0, 6 * sizeof(int), c->st));
     SweepParams p{};
     p.part = part;
     p.side = Lr.side; p.s = Lr.s; p.nb = Lr.nb; p.nca = nca; p.ncells = ncells;
@@ -213,16 +222,39 @@ int sweep(dd_ctx* c) {
     p.alpha = part == 1 ? c->alphaA : c->alphaB;
     p.mu = Lr.mu; p.logmu = Lr.logmu; p.mass_i = Lr.mass;
     p.out = c->cellout;
-    p.deferred = c->deferred; p.n_deferred = c->counters; p.work_counter = c->counters + 1;
-    p.overflow = c->counters + 2;
+    p.overflow = c->counters + 6;
     SweepEvents ev;
     int rc = alloc_events(c, ev);
     if (rc) return rc;
     CK(cudaEventRecord(ev.e[0], c->st));
-    p.mode = 0; p.bcap = c->bcap_main;
-    CK(launch_k1(p, ncells, c->smem_main, c->st));
-    p.mode = 1; p.bcap = c->bcap_big;
-    CK(launch_k1(p, std::min(c->grid_big, ncells), c->smem_big, c->st));
+    const int bhuge = std::min(Lr.side, c->bcap_huge);
+    CK(launch_k0(p, c->bcap_main, c->bcap_big, c->lists, c->counters, c->ncell_max, c->st));
+    CK(cudaEventRecord(c->ev_fork, c->st));
+    CK(cudaStreamWaitEvent(c->st_t[0], c->ev_fork, 0));
+    CK(cudaStreamWaitEvent(c->st_t[1], c->ev_fork, 0));
+    {   // tier 2: largest boxes first, arrays in L2-resident global slices
+        SweepParams q = p;
+        q.bcap = bhuge;
+        q.list_in = c->lists + 2 * c->ncell_max; q.n_in = c->counters + 2; q.work_counter = c->counters + 5;
+        q.gscratch = c->huge; q.gslice = c->huge_slice;
+        CK(launch_k1(q, 2, std::min(c->grid_huge, ncells), 0, c->st_t[1]));
+    }
+    {   // tier 1: one big-SMEM CTA per SM
+        SweepParams q = p;
+        q.bcap = c->bcap_big;
+        q.list_in = c->lists + c->ncell_max; q.n_in = c->counters + 1; q.work_counter = c->counters + 4;
+        CK(launch_k1(q, 1, std::min(c->grid_big, ncells), c->smem_big, c->st_t[0]));
+    }
+    {   // tier 0: the bulk, several CTAs per SM
+        SweepParams q = p;
+        q.bcap = c->bcap_main;
+        q.list_in = c->lists; q.n_in = c->counters; q.work_counter = c->counters + 3;
+        CK(launch_k1(q, 0, std::min(ncells, c->grid_big * 8), c->smem_main, c->st));
+    }
+    CK(cudaEventRecord(c->ev_join[0], c->st_t[0]));
+    CK(cudaEventRecord(c->ev_join[1], c->st_t[1]));
+    CK(cudaStreamWaitEvent(c->st, c->ev_join[0], 0));
+    CK(cudaStreamWaitEvent(c->st, c->ev_join[1], 0));
     CK(cudaEventRecord(ev.e[1], c->st));
     // K2: deterministic compaction of the new boxes into the pool
     const int nb2 = Lr.nb * Lr.nb;
@@ -230,11 +262,11 @@ int sweep(dd_ctx* c) {
     CK(launch_copy_boxes(c->box, c->off, c->off2, c->scratch, c->pool, nb2, c->cap, c->st));
     std::swap(c->off, c->off2);
     // K3: fixed-order sweep statistics
-    CK(launch_reduce_stats(c->cellout, ncells, c->d_last, c->d_tot, c->d_total + 1, c->counters,
-                           c->counters + 2, c->st));
+    CK(launch_reduce_stats(c->cellout, ncells, c->d_last, c->d_tot, c->d_total + 1, c->counters + 1,
+                           c->counters + 6, c->counters + 2, c->st));
     CK(cudaEventRecord(ev.e[2], c->st));
     c->pending.push_back(ev);
-    c->launches_pending += 5;
+    c->launches_pending += 7;
     c->half_index++;
     c->last_part = part;
     if (c->pending.size() > 512) return harvest(c);
@@ -249,7 +281,7 @@ int product_init(dd_ctx* c) {
     const size_t n2 = (size_t)c->L[c->n_layers - 1].side * c->L[c->n_layers - 1].side;
     CK(cudaMemsetAsync(c->alphaA, 0, n2 * sizeof(double), c->st));
     CK(cudaMemsetAsync(c->alphaB, 0, n2 * sizeof(double), c->st));
-    CK(cudaMemsetAsync(c->counters, 0, 3 * sizeof(int), c->st));
+    CK(cudaMemsetAsync(c->counters, 0, 8 * sizeof(int), c->st));
     c->half_index = 0;
     c->last_part = 0;
     return DD_OK;
@@ -260,10 +292,15 @@ void free_all(dd_ctx* c) {
         cudaFree(c->L[k].mu); cudaFree(c->L[k].nu); cudaFree(c->L[k].logmu); cudaFree(c->L[k].mass);
     }
     void* ptrs[] = {c->alphaA, c->alphaB, c->box, c->box2, c->off, c->off2, c->pool, c->scratch,
-                    c->bump, c->deferred, c->counters, c->cellout, c->d_total, c->d_last, c->d_tot,
+                    c->bump, c->lists, c->huge, c->counters, c->cellout, c->d_total, c->d_last, c->d_tot,
                     c->eval_scratch, c->eval_res, c->d_sums, c->yacc, c->partial};
     for (void* q : ptrs) if (q) cudaFree(q);
     for (auto& ev : c->pending) for (int k = 0; k < 3; ++k) cudaEventDestroy(ev.e[k]);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    for (int k = 0; k < 2; ++k) {
+        if (c->ev_join[k]) cudaEventDestroy(c->ev_join[k]);
+        if (c->st_t[k]) cudaStreamDestroy(c->st_t[k]);
+    }
     for (auto& ev : c->free_events) for (int k = 0; k < 3; ++k) cudaEventDestroy(ev.e[k]);
     if (c->own_stream && c->st) cudaStreamDestroy(c->st);
 }
@@ -361,7 +398,7 @@ void fill_stats(const DevStats& d, dd_sweep_stats* s) {
     s->err_x_sum = d.err_sum;
     s->entries = d.entries;
     s->mufu_ops = d.mufu;
-    s->big_cells = d.deferred;
+    s->big_cells = d.deferred + d.huge;
     s->max_box = d.max_box;
     s->reserved_i = (int)std::min<long long>(d.fallbacks, 2147483647LL);
 }
@@ -518,8 +555,19 @@ int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, d
     CK(cudaMalloc(&c->scratch, (size_t)c->cap * sizeof(double)));
     CK(cudaMalloc(&c->bump, sizeof(unsigned long long)));
     c->ncell_max = (nbmax / 2 + 1) * (nbmax / 2 + 1);
-    CK(cudaMalloc(&c->deferred, (size_t)c->ncell_max * sizeof(int)));
-    CK(cudaMalloc(&c->counters, 4 * sizeof(int)));
+    CK(cudaMalloc(&c->lists, (size_t)3 * c->ncell_max * sizeof(int)));
+    CK(cudaMalloc(&c->counters, 8 * sizeof(int)));
+    CK(cudaMemsetAsync(c->counters, 0, 8 * sizeof(int), c->st));
+    // tier-2 scratch: a K1 layout for Y boxes up to bcap_huge, one slice per CTA
+    c->bcap_huge = std::min(n, c->opt.reserved[1] > 0 ? c->opt.reserved[1] : 512);
+    c->huge_slice = (long long)((k1_smem_bytes_host(F.s, c->bcap_huge) + 255) & ~(size_t)255);
+    c->grid_huge = prop.multiProcessorCount;
+    CK(cudaMalloc(&c->huge, (size_t)c->huge_slice * c->grid_huge));
+    for (int k = 0; k < 2; ++k) {
+        CK(cudaStreamCreateWithFlags(&c->st_t[k], cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev_join[k], cudaEventDisableTiming));
+    }
+    CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK(cudaMalloc(&c->cellout, (size_t)c->ncell_max * sizeof(CellOut)));
     CK(cudaMalloc(&c->d_total, 2 * sizeof(long long)));
     CK(cudaMalloc(&c->d_last, sizeof(DevStats)));
@@ -620,7 +668,7 @@ int dd_get_stats(dd_ctx* c, dd_sweep_stats* s) {
     fill_stats(d, s);
     s->ms = c->ms_last;
     s->solve_ms = c->solve_ms_last;
-    s->launches = 5;
+    s->launches = 7;
     if (d.failed) {
         set_err(c, "%d cells did not converge within max_inner_iter", d.failed);
         return DD_ENOCONV;

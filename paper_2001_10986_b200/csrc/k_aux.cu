@@ -113,7 +113,7 @@ __global__ void k_copy_boxes(const int4* __restrict__ box, const long long* __re
 // (one block of 1024 threads; thread t owns cells t, t+1024, ... in order).
 __global__ void k_reduce_stats(const CellOut* __restrict__ out, int ncells, DevStats* last, DevStats* tot,
                                const long long* __restrict__ entries, const int* __restrict__ n_deferred,
-                               const int* __restrict__ overflow) {
+                               const int* __restrict__ overflow, const int* __restrict__ n_huge) {
     __shared__ double s_err[1024], s_mufu[1024];
     __shared__ long long s_it[1024], s_fb[1024];
     __shared__ int s_max[1024], s_fail[1024], s_box[1024];
@@ -155,6 +155,7 @@ __global__ void k_reduce_stats(const CellOut* __restrict__ out, int ncells, DevS
         L.mufu = s_mufu[0];
         L.fallbacks = s_fb[0];
         L.deferred = *n_deferred;
+        L.huge = *n_huge;
         L.max_box = s_box[0];
         L.overflow = *overflow;
         L.entries = *entries;
@@ -167,6 +168,7 @@ __global__ void k_reduce_stats(const CellOut* __restrict__ out, int ncells, DevS
         tot->mufu += L.mufu;
         tot->fallbacks += L.fallbacks;
         tot->deferred += L.deferred;
+        tot->huge += L.huge;
         tot->max_box = max(tot->max_box, L.max_box);
         tot->overflow |= L.overflow;
         tot->entries = L.entries;
@@ -422,8 +424,8 @@ cudaError_t launch_copy_boxes(const int4* box, const long long* srcoff, const lo
 }
 cudaError_t launch_reduce_stats(const CellOut* out, int ncells, DevStats* last, DevStats* tot,
                                 const long long* entries, const int* n_deferred, const int* overflow,
-                                cudaStream_t st) {
-    k_reduce_stats<<<1, 1024, 0, st>>>(out, ncells, last, tot, entries, n_deferred, overflow);
+                                const int* n_huge, cudaStream_t st) {
+    k_reduce_stats<<<1, 1024, 0, st>>>(out, ncells, last, tot, entries, n_deferred, overflow, n_huge);
     LAUNCH_CHECK(); return cudaSuccess;
 }
 cudaError_t launch_refine(const int4* cbox, const long long* coff, const double* cpool, int4* fbox,

@@ -690,6 +690,30 @@ int dd_get_totals(dd_ctx* c, dd_sweep_stats* s) {
     return DD_OK;
 }
 
+int dd_get_cell_stats(dd_ctx* c, int* iters, int* box_side, double* mufu_ops, int max_cells) {
+    if (!c || max_cells < 0) return -DD_EINVAL;
+    int rc = harvest(c);
+    if (rc) return -rc;
+    const Layer& Lr = c->L[c->cur];
+    const int part = c->last_part ? c->last_part : 1;
+    const int nca = cells_axis(Lr.nb, part);
+    const int ncells = c->last_part ? nca * nca : 0;
+    const int m = std::min(ncells, max_cells);
+    if (m > 0) {
+        std::vector<CellOut> h(m);
+        if (cudaMemcpy(h.data(), c->cellout, m * sizeof(CellOut), cudaMemcpyDeviceToHost) != cudaSuccess) {
+            set_err(c, "dd_get_cell_stats: copy failed");
+            return -DD_ECUDA;
+        }
+        for (int k = 0; k < m; ++k) {
+            if (iters) iters[k] = h[k].iters;
+            if (box_side) box_side[k] = h[k].box;
+            if (mufu_ops) mufu_ops[k] = h[k].mufu;
+        }
+    }
+    return ncells;
+}
+
 int dd_reset_totals(dd_ctx* c) {
     if (!c) return DD_EINVAL;
     int rc = harvest(c);

@@ -23,7 +23,7 @@ PLAN_BASIC_MARGINALS, PLAN_COO = 0, 1
 # every symbol include/dd.h declares (checked by tests/test_abi.py)
 EXPORTS = ["dd_init", "dd_iterate", "dd_set_eps", "dd_refine", "dd_run_schedule", "dd_reset",
            "dd_primal_cost", "dd_marginal_error", "dd_fetch_plan", "dd_get_stats", "dd_get_totals",
-           "dd_reset_totals", "dd_get_state_info", "dd_get_state", "dd_set_state",
+           "dd_reset_totals", "dd_get_cell_stats", "dd_get_state_info", "dd_get_state", "dd_set_state",
            "dd_build_schedule", "dd_measure_mufu_peak", "dd_synchronize", "dd_free",
            "dd_last_error", "dd_version"]
 
@@ -74,6 +74,7 @@ def lib():
         L.dd_get_stats.argtypes = [p, C.POINTER(SweepStats)]
         L.dd_get_totals.argtypes = [p, C.POINTER(SweepStats)]
         L.dd_reset_totals.argtypes = [p]
+        L.dd_get_cell_stats.argtypes = [p, p, p, p, i]
         L.dd_get_state_info.argtypes = [p, C.POINTER(StateInfo)]
         L.dd_get_state.argtypes = [p, p, p, p, p, p]
         L.dd_set_state.argtypes = [p, i, ll, i, p, p, p, ll, p, p]
@@ -208,6 +209,17 @@ class DD:
 
     def reset_totals(self):
         return self._check(lib().dd_reset_totals(self._h), "reset_totals")
+
+    def cell_stats(self):
+        """Per composite cell of the last sweep: (iters, box_side, mufu_ops) arrays."""
+        n = lib().dd_get_cell_stats(self._h, None, None, None, 0)
+        if n < 0:
+            raise RuntimeError(f"dd_get_cell_stats rc={-n}: {self.last_error()}")
+        it = np.zeros(max(n, 1), np.int32)
+        bx = np.zeros(max(n, 1), np.int32)
+        mf = np.zeros(max(n, 1), np.float64)
+        lib().dd_get_cell_stats(self._h, it.ctypes.data, bx.ctypes.data, mf.ctypes.data, n)
+        return it[:n], bx[:n], mf[:n]
 
     def state_info(self):
         inf = StateInfo()

@@ -75,7 +75,9 @@ typedef struct {                /* zero-initialised fields take the defaults */
     int device;                 /* CUDA device ordinal */
     long long pool_capacity;    /* nu_i pool entries per buffer; 0 -> 48 * N^2 + 2^20 */
     void* stream;               /* cudaStream_t to use, or NULL */
-    int reserved[8];
+    int reserved[8];            /* [0] > 0: box-side cap of the SMEM tier (tier 0);
+                                   [1] > 0: box-side cap of the 2-CTA/SM fused tier (tier 1);
+                                   testing knobs that route cells to the other K1 tiers */
 } dd_options;
 
 typedef struct {                /* one sweep (or accumulated totals) */

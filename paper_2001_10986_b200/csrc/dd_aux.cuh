@@ -34,9 +34,10 @@ struct EvalParams {
     double* coo_m;
 };
 
-size_t k1_smem_bytes_host(int s, int bcap);
+size_t k1_smem_bytes_host(int s, int bcap, bool big = false, int nwarps = 0);
 cudaError_t launch_k1(const SweepParams& p, int tier, int grid, size_t smem, cudaStream_t st);
-cudaError_t launch_k0(const SweepParams& p, int b0, int b1, int* lists, int* counts, int ncap, cudaStream_t st);
+cudaError_t launch_k0(const SweepParams& p, int b0, int b1, int* lists, int* counts, int ncap, int* bside,
+                      int* sorted, cudaStream_t st);
 cudaError_t launch_pool2x2(const double* fine, double* coarse, int sc, cudaStream_t st);
 cudaError_t launch_log(const double* x, double* lx, long long n, cudaStream_t st);
 cudaError_t launch_mass_i(const double* mu, double* mass, int side, int s, int nb, cudaStream_t st);

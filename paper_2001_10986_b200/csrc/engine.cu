@@ -55,11 +55,13 @@ struct dd_ctx {
     long long cap = 0;
     // sweep plumbing
     unsigned long long* bump = nullptr;
-    int* lists = nullptr;           // tier lists [3][ncell_max] (K0)
+    int* lists = nullptr;           // tier lists [3][ncell_max] (K0) + LPT-sorted tiers 1, 2 [2][ncell_max]
+    int* bside = nullptr;           // union Y-box side per cell (K0)
     int* counters = nullptr;        // [0..2] tier counts, [3..5] work counters, [6] overflow
-    unsigned char* huge = nullptr;  // global-memory slices of the tier-2 (largest box) path
-    long long huge_slice = 0;
-    int grid_huge = 0, bcap_huge = 512;
+    unsigned char* slices[2] = {nullptr, nullptr};   // BIG tiers: per-CTA global slices (log nu_cell, ACC)
+    long long slice_bytes[2] = {0, 0};
+    int slice_cap[2] = {0, 0};      // box side the slices were sized for
+    int grid_t[2] = {0, 0};         // persistent grid of tiers 1, 2
     cudaStream_t st_t[2] = {nullptr, nullptr};   // tier 1 / tier 2 streams
     cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
     CellOut* cellout = nullptr;
@@ -67,8 +69,8 @@ struct dd_ctx {
     DevStats* d_last = nullptr;
     DevStats* d_tot = nullptr;
     int ncell_max = 0;
-    int bcap_main = 32, bcap_big = 32;
-    size_t smem_main = 0, smem_big = 0;
+    int bcap_main = 32, bcap_big = 32, bcap_big2 = 32;
+    size_t smem_main = 0, smem_big = 0, smem_big2 = 0;
     int grid_big = 148;
     // evaluation scratch
     double* eval_scratch = nullptr;
@@ -176,29 +178,46 @@ int check_overflow(dd_ctx* c) {
         return DD_ENOMEM;
     }
     if (ov & 2) {
-        set_err(c, "a composite cell's Y box exceeds the largest supported box side (%d)", c->bcap_huge);
+        set_err(c, "a composite cell's Y box exceeds the largest supported box side (%d)", c->bcap_big2);
         return DD_ENOMEM;
     }
     return DD_OK;
 }
 
-void choose_caps(dd_ctx* c, int s) {
-    // tier 0: SMEM for union Y boxes <= bcap_main (several CTAs per SM);
-    // tier 1: one CTA per SM with up to ~220 KB SMEM; tier 2: global slices
+// Box-side capacities of the three K1 tiers for basic cell side s:
+//   tier 0 (SMEM path, 256 threads, 3 CTAs/SM): union Y box <= bcap_main;
+//   tier 1 (BIG path, 256 threads, 2 CTAs/SM): <= bcap_big (<= kCap1);
+//   tier 2 (BIG path, 512 threads, 1 CTA/SM):  <= bcap_big2 (<= kCap2).
+constexpr int kCap1 = 320, kCap2 = 704;
+constexpr size_t kSmem1 = 110 * 1024, kSmem2 = 220 * 1024;
+void tier_caps(int s, int opt_main, int opt_big, int* b0, int* b1, int* b2) {
     int want = (s <= 4) ? 32 : 40;
-    if (c->opt.reserved[0] > 0) want = c->opt.reserved[0];
+    if (opt_main > 0) want = opt_main;
     if (want < 2 * s + 2) want = 2 * s + 2;
-    c->bcap_main = want;
-    c->smem_main = k1_smem_bytes_host(s, want);
+    *b0 = want;
     int big = want;
-    while (k1_smem_bytes_host(s, big + 1) <= 216 * 1024) ++big;
-    c->bcap_big = big;
-    c->smem_big = k1_smem_bytes_host(s, big);
+    while (big < kCap1 && k1_smem_bytes_host(s, big + 1, true, 8) <= kSmem1) ++big;
+    int big2 = big;
+    if (opt_big > 0 && opt_big >= want && opt_big < big) big = opt_big;   // testing: force tier 2
+    *b1 = big;
+    while (big2 < kCap2 && k1_smem_bytes_host(s, big2 + 1, true, 16) <= kSmem2) ++big2;
+    *b2 = big2;
+}
+
+void choose_caps(dd_ctx* c, int s) {
+    int b0, b1, b2;
+    tier_caps(s, c->opt.reserved[0], c->opt.reserved[1], &b0, &b1, &b2);
+    c->bcap_main = b0;
+    c->smem_main = k1_smem_bytes_host(s, b0);
+    c->bcap_big = std::min(b1, c->slice_cap[0]);
+    c->smem_big = k1_smem_bytes_host(s, c->bcap_big, true, 8);
+    c->bcap_big2 = std::min(b2, c->slice_cap[1]);
+    c->smem_big2 = k1_smem_bytes_host(s, c->bcap_big2, true, 16);
 }
 
 // One sweep (Alg. 2 lines 6-14) over the partition selected by the parity of
 // the half-iteration index (line 7: odd l -> A).
-//   K0 classify cells by union Y-box side -> tier lists
+//   K0 classify cells by union Y-box side -> tier lists (big tiers LPT-sorted)
 //   tiers 2 | 1 | 0 run concurrently on three streams (fork/join events)
 //   K2 deterministic compaction, K3 fixed-order statistics
 int sweep(dd_ctx* c) {
@@ -227,23 +246,24 @@ int sweep(dd_ctx* c) {
     int rc = alloc_events(c, ev);
     if (rc) return rc;
     CK(cudaEventRecord(ev.e[0], c->st));
-    const int bhuge = std::min(Lr.side, c->bcap_huge);
-    CK(launch_k0(p, c->bcap_main, c->bcap_big, c->lists, c->counters, c->ncell_max, c->st));
+    int* sorted = c->lists + 3 * (size_t)c->ncell_max;
+    CK(launch_k0(p, c->bcap_main, c->bcap_big, c->lists, c->counters, c->ncell_max, c->bside, sorted, c->st));
     CK(cudaEventRecord(c->ev_fork, c->st));
     CK(cudaStreamWaitEvent(c->st_t[0], c->ev_fork, 0));
     CK(cudaStreamWaitEvent(c->st_t[1], c->ev_fork, 0));
-    {   // tier 2: largest boxes first, arrays in L2-resident global slices
+    {   // tier 2: the largest boxes (LPT order), fused path, 512 threads, 1 CTA/SM
         SweepParams q = p;
-        q.bcap = bhuge;
-        q.list_in = c->lists + 2 * c->ncell_max; q.n_in = c->counters + 2; q.work_counter = c->counters + 5;
-        q.gscratch = c->huge; q.gslice = c->huge_slice;
-        CK(launch_k1(q, 2, std::min(c->grid_huge, ncells), 0, c->st_t[1]));
+        q.bcap = c->bcap_big2;
+        q.list_in = sorted + c->ncell_max; q.n_in = c->counters + 2; q.work_counter = c->counters + 5;
+        q.gscratch = c->slices[1]; q.gslice = c->slice_bytes[1];
+        CK(launch_k1(q, 2, std::min(c->grid_t[1], ncells), c->smem_big2, c->st_t[1]));
     }
-    {   // tier 1: one big-SMEM CTA per SM
+    {   // tier 1: fused path, 256 threads, 2 CTAs/SM (LPT order)
         SweepParams q = p;
         q.bcap = c->bcap_big;
-        q.list_in = c->lists + c->ncell_max; q.n_in = c->counters + 1; q.work_counter = c->counters + 4;
-        CK(launch_k1(q, 1, std::min(c->grid_big, ncells), c->smem_big, c->st_t[0]));
+        q.list_in = sorted; q.n_in = c->counters + 1; q.work_counter = c->counters + 4;
+        q.gscratch = c->slices[0]; q.gslice = c->slice_bytes[0];
+        CK(launch_k1(q, 1, std::min(c->grid_t[0], ncells), c->smem_big, c->st_t[0]));
     }
     {   // tier 0: the bulk, several CTAs per SM
         SweepParams q = p;
@@ -266,7 +286,7 @@ int sweep(dd_ctx* c) {
                            c->counters + 6, c->counters + 2, c->st));
     CK(cudaEventRecord(ev.e[2], c->st));
     c->pending.push_back(ev);
-    c->launches_pending += 7;
+    c->launches_pending += 8;
     c->half_index++;
     c->last_part = part;
     if (c->pending.size() > 512) return harvest(c);
@@ -292,7 +312,7 @@ void free_all(dd_ctx* c) {
         cudaFree(c->L[k].mu); cudaFree(c->L[k].nu); cudaFree(c->L[k].logmu); cudaFree(c->L[k].mass);
     }
     void* ptrs[] = {c->alphaA, c->alphaB, c->box, c->box2, c->off, c->off2, c->pool, c->scratch,
-                    c->bump, c->lists, c->huge, c->counters, c->cellout, c->d_total, c->d_last, c->d_tot,
+                    c->bump, c->lists, c->bside, c->slices[0], c->slices[1], c->counters, c->cellout, c->d_total, c->d_last, c->d_tot,
                     c->eval_scratch, c->eval_res, c->d_sums, c->yacc, c->partial};
     for (void* q : ptrs) if (q) cudaFree(q);
     for (auto& ev : c->pending) for (int k = 0; k < 3; ++k) cudaEventDestroy(ev.e[k]);
@@ -555,14 +575,26 @@ int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, d
     CK(cudaMalloc(&c->scratch, (size_t)c->cap * sizeof(double)));
     CK(cudaMalloc(&c->bump, sizeof(unsigned long long)));
     c->ncell_max = (nbmax / 2 + 1) * (nbmax / 2 + 1);
-    CK(cudaMalloc(&c->lists, (size_t)3 * c->ncell_max * sizeof(int)));
+    CK(cudaMalloc(&c->lists, (size_t)5 * c->ncell_max * sizeof(int)));
+    CK(cudaMalloc(&c->bside, (size_t)c->ncell_max * sizeof(int)));
     CK(cudaMalloc(&c->counters, 8 * sizeof(int)));
     CK(cudaMemsetAsync(c->counters, 0, 8 * sizeof(int), c->st));
-    // tier-2 scratch: a K1 layout for Y boxes up to bcap_huge, one slice per CTA
-    c->bcap_huge = std::min(n, c->opt.reserved[1] > 0 ? c->opt.reserved[1] : 512);
-    c->huge_slice = (long long)((k1_smem_bytes_host(F.s, c->bcap_huge) + 255) & ~(size_t)255);
-    c->grid_huge = prop.multiProcessorCount;
-    CK(cudaMalloc(&c->huge, (size_t)c->huge_slice * c->grid_huge));
+    // BIG tiers: one global slice per persistent CTA holding log nu_cell
+    // (b^2 float2) and the extraction partial sums (b^2 float4), sized for
+    // the largest tier capacity over the layers (box sides never exceed the side)
+    for (int k = 0; k < nl; ++k) {
+        int b0, b1, b2;
+        tier_caps(c->L[k].s, c->opt.reserved[0], c->opt.reserved[1], &b0, &b1, &b2);
+        c->slice_cap[0] = std::max(c->slice_cap[0], std::min(b1, c->L[k].side));
+        c->slice_cap[1] = std::max(c->slice_cap[1], std::min(b2, c->L[k].side));
+    }
+    c->grid_t[0] = 2 * prop.multiProcessorCount;
+    c->grid_t[1] = prop.multiProcessorCount;
+    for (int t = 0; t < 2; ++t) {
+        const long long b = c->slice_cap[t];
+        c->slice_bytes[t] = (((b * b * (long long)sizeof(float2) + 255) & ~255LL) + b * b * (long long)sizeof(float4) + 255) & ~255LL;
+        CK(cudaMalloc(&c->slices[t], (size_t)c->slice_bytes[t] * c->grid_t[t]));
+    }
     for (int k = 0; k < 2; ++k) {
         CK(cudaStreamCreateWithFlags(&c->st_t[k], cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&c->ev_join[k], cudaEventDisableTiming));

@@ -42,12 +42,18 @@ struct K1Lay {
     float2* LNU;  // [br][bc]  log nu_cell (hi, lo2)
     float* CT;    // cost table C(d) = d^2 / kappa, d in [-OFF, OFF]
     double* red;  // reduction scratch (64)
+    float2* gbuf; // BIG: per-warp G rows of the fused Y2+X1 pass [warp][kGbufPerWarp]
 };
 
-__host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
-__host__ __device__ inline int k1_ct_off(int s, int bcap) { return (2 * s > bcap ? 2 * s : bcap) + 8; }
+// BIG mode (fused Y2+X1): G is never stored as
+// a b^2 array; log nu_cell (b^2 float2) and the extraction partial sums
+// (b^2 float4) live in an L2-resident global slice per CTA.
+constexpr int kGbufPerWarp = 288;   // max over (NQ, RG) of RG * YS * (SUB + 1)
 
-__host__ __device__ inline void k1_sizes(int s, int bcap, size_t* sz) {
+__host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
+__host__ __device__ inline int k1_ct_off(int s, int bcap) { return (2 * s > bcap ? 2 * s : bcap) + 24; }
+
+__host__ __device__ inline void k1_sizes(int s, int bcap, size_t* sz, bool big = false, int nwarps = 0) {
     const size_t A = 2 * s, pA = odd_pitch(2 * s), pB = odd_pitch(bcap), B = bcap;
     sz[0] = align16(A * pA * 8);                        // FX
     sz[1] = align16(A * pA * 8);                        // FXn
@@ -55,22 +61,23 @@ __host__ __device__ inline void k1_sizes(int s, int bcap, size_t* sz) {
     sz[3] = align16(A * A * 4);                         // MU
     sz[4] = align16(B * pA * 8);                        // Tt
     sz[5] = align16((A * pB > B * pA ? A * pB : B * pA) * 8);   // Ut / W
-    sz[6] = align16(B * pB * 8);                        // G   } ACC (16 B per y) overlays
-    sz[7] = align16(B * B * 8);                         // LNU }
+    sz[6] = big ? 0 : align16(B * pB * 8);              // G   } ACC (16 B per y) overlays
+    sz[7] = big ? 0 : align16(B * B * 8);               // LNU }
     sz[8] = align16((2 * k1_ct_off(s, bcap) + 8) * 4);  // CT
     sz[9] = 64 * 8;                                     // red
+    sz[10] = big ? (size_t)nwarps * kGbufPerWarp * 8 : 0;   // gbuf
 }
 
-__host__ __device__ inline size_t k1_smem_bytes(int s, int bcap) {
-    size_t sz[10], b = 0;
-    k1_sizes(s, bcap, sz);
-    for (int k = 0; k < 10; ++k) b += sz[k];
+__host__ __device__ inline size_t k1_smem_bytes(int s, int bcap, bool big = false, int nwarps = 0) {
+    size_t sz[11], b = 0;
+    k1_sizes(s, bcap, sz, big, nwarps);
+    for (int k = 0; k < 11; ++k) b += sz[k];
     return b;
 }
 
-__device__ inline K1Lay k1_carve(unsigned char* base, int s, int bcap) {
-    size_t sz[10];
-    k1_sizes(s, bcap, sz);
+__device__ inline K1Lay k1_carve(unsigned char* base, int s, int bcap, bool big = false, int nwarps = 0) {
+    size_t sz[11];
+    k1_sizes(s, bcap, sz, big, nwarps);
     K1Lay L;
     size_t o = 0;
     L.FX = (float2*)(base + o);  o += sz[0];
@@ -82,7 +89,8 @@ __device__ inline K1Lay k1_carve(unsigned char* base, int s, int bcap) {
     L.G = (float2*)(base + o);   o += sz[6];
     L.LNU = (float2*)(base + o); o += sz[7];
     L.CT = (float*)(base + o);   o += sz[8];
-    L.red = (double*)(base + o);
+    L.red = (double*)(base + o); o += sz[9];
+    L.gbuf = (float2*)(base + o);
     return L;
 }
 
@@ -381,10 +389,258 @@ __device__ __forceinline__ void lse_pass(const K1Lay& L, const Dims& d, const Gr
     }
 }
 
-// ----------------------------------------------------------- the solve --
+// ------------------------------------------------- BIG: fused Y2 + X1 pass --
+// For every Y row y1 (row groups of RG rows per warp, no block barrier):
+//   phase A (lane <-> y2 of a 32-column chunk):
+//     G(y1, y2) = log nu_cell(y1, y2) - LSE_x1[T(x1, y2) - C(x1 - y1)]
+//     (exact max over the AR terms held in registers; the T column is reused
+//     by the RG rows of the group)
+//   phase B (lane <-> (row r, x2 quad, y2 sub-slice)):
+//     U(y1, x2) += sum_{y2 in chunk} exp(G(y1, y2) - C(y2 - x2) - S(y1, x2))
+//     (speculative stabiliser S = previous U, sliding cost window; exact
+//     two-pass max on the first iteration or when the window check fails)
+// G lives only in a per-warp buffer of one chunk; U is written to Ut[x2][y1]
+// for the X2 pass.  Algorithmic exps: ar br bc (phase A) + br bc ac (phase B)
+// = the Y2 and X1 passes of the separable scheme.
+template <int NT, int AR, int NQ, int RG>
+__device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all,
+                                           const float2* __restrict__ LNUg, int& fallbacks, int& nonfinite) {
+    constexpr int YS = 32 / (RG * NQ);      // phase-B lanes sharing one output (y2 split)
+    constexpr int SUB = 32 / YS;            // y2 per phase-B lane slice of a chunk
+    constexpr int PR = YS * (SUB + 1);      // gbuf row pitch (float2), conflict-free
+    constexpr int NWA = AR + RG - 1;        // phase-A cost window
+    static_assert(RG * PR <= kGbufPerWarp, "gbuf");
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float2* gb = L.gbuf + warp * kGbufPerWarp;
+    const int ngroups = (d.br + RG - 1) / RG;
+    const int rB = lane / (NQ * YS);
+    const int qB = (lane / YS) % NQ;
+    const int hB = lane % YS;
+    const int x2b = 4 * qB;
+    const int gidxA = (lane / SUB) * (SUB + 1) + lane % SUB;   // phase-A write slot of this lane's y2
+    const float2 L2E2 = make_float2(kL2E, kL2E);
+
+    for (int grp = warp; grp < ngroups; grp += NT / 32) {
+        const int y1b = grp * RG;
+        const int y1B = y1b + rB;
+        const bool rvalid = y1B < d.br;
+        // phase-A cost window: C(x1 - (y1b + r)) = wA[x1 - r + RG - 1]
+        float wA[NWA];
+        {
+            const float* cw = L.CT + d.off - y1b - (RG - 1);
+#pragma unroll
+            for (int m = 0; m < NWA; ++m) wA[m] = cw[m];
+        }
+        auto phaseA = [&](int c0) {
+            const int y2 = c0 + lane;
+            const bool vy = y2 < d.bc;
+            float th[AR], tl[AR];
+#pragma unroll
+            for (int x = 0; x < AR; ++x) {
+                const float2 t = (vy && x < d.ar) ? L.Tt[y2 * d.pT + x] : make_float2(-INFINITY, 0.f);
+                th[x] = t.x;
+                tl[x] = t.y;
+            }
+            float2 ln[RG];
+#pragma unroll
+            for (int r = 0; r < RG; ++r)
+                ln[r] = (vy && y1b + r < d.br) ? LNUg[(y1b + r) * d.bc + y2] : make_float2(-INFINITY, 0.f);
+#pragma unroll
+            for (int r = 0; r < RG; ++r) {
+                float2 g = make_float2(-INFINITY, 0.f);
+                if (ln[r].x != -INFINITY) {
+                    float t[AR];
+#pragma unroll
+                    for (int x = 0; x < AR; x += 2) {
+                        const float2 tt = __fadd2_rn(make_float2(th[x], th[x + 1]),
+                                                     make_float2(-wA[x - r + RG - 1], -wA[x + 1 - r + RG - 1]));
+                        t[x] = tt.x;
+                        t[x + 1] = tt.y;
+                    }
+                    float M = t[0];
+#pragma unroll
+                    for (int x = 1; x + 1 < AR; x += 2) M = fmax3f(M, t[x], t[x + 1]);
+                    if (AR % 2 == 0) M = fmaxf(M, t[AR - 1]);
+                    if (M > -INFINITY) {
+                        float2 s2 = make_float2(0.f, 0.f);
+                        const float2 nM = make_float2(-M, -M);
+#pragma unroll
+                        for (int x = 0; x < AR; x += 2) {
+                            float2 a = __fadd2_rn(make_float2(t[x], t[x + 1]), nM);
+                            a = __ffma2_rn(a, L2E2, make_float2(tl[x], tl[x + 1]));
+                            s2 = __fadd2_rn(s2, make_float2(ex2f(a.x), ex2f(a.y)));
+                        }
+                        float lh, ll;
+                        ln_split(s2.x + s2.y, gq, lh, ll);
+                        g = make_float2(ln[r].x - (M + lh), ln[r].y - ll);
+                    } else {
+                        nonfinite = 1;       // nu_cell(y) > 0 unreachable from X
+                    }
+                }
+                gb[r * PR + gidxA] = g;
+            }
+        };
+        // phase B over one chunk: MAXMODE -> running max, else sums with S
+        auto phaseB = [&](int c0, bool maxmode, const float* S, float* A) {
+            const int ybase = c0 + hB * SUB;
+            const int nk = min(SUB, d.bc - ybase);
+            const float2* grow = gb + rB * PR + hB * (SUB + 1);
+            const float* ctp = L.CT + d.off + ybase - x2b;    // C(y2 - x2b - j) = ctp[k - j]
+            float c1 = ctp[-1], c2 = ctp[-2], c3 = ctp[-3];
+            if (maxmode) {
+                for (int k = 0; k < nk; ++k) {
+                    const float c0v = ctp[k];
+                    const float gx = grow[k].x;
+                    A[0] = fmaxf(A[0], gx - c0v); A[1] = fmaxf(A[1], gx - c1);
+                    A[2] = fmaxf(A[2], gx - c2); A[3] = fmaxf(A[3], gx - c3);
+                    c3 = c2; c2 = c1; c1 = c0v;
+                }
+            } else {
+                const float2 nS01 = make_float2(-S[0], -S[1]), nS23 = make_float2(-S[2], -S[3]);
+                float2 a01 = make_float2(A[0], A[1]), a23 = make_float2(A[2], A[3]);
+#pragma unroll 2
+                for (int k = 0; k < nk; ++k) {
+                    const float c0v = ctp[k];
+                    const float2 g = grow[k];
+                    float2 t01 = __fadd2_rn(make_float2(g.x, g.x), make_float2(-c0v, -c1));
+                    float2 t23 = __fadd2_rn(make_float2(g.x, g.x), make_float2(-c2, -c3));
+                    t01 = __fadd2_rn(t01, nS01);
+                    t23 = __fadd2_rn(t23, nS23);
+                    t01 = __ffma2_rn(t01, L2E2, make_float2(g.y, g.y));
+                    t23 = __ffma2_rn(t23, L2E2, make_float2(g.y, g.y));
+                    a01 = __fadd2_rn(a01, make_float2(ex2f(t01.x), ex2f(t01.y)));
+                    a23 = __fadd2_rn(a23, make_float2(ex2f(t23.x), ex2f(t23.y)));
+                    c3 = c2; c2 = c1; c1 = c0v;
+                }
+                A[0] = a01.x; A[1] = a01.y; A[2] = a23.x; A[3] = a23.y;
+            }
+        };
+        // speculative stabilisers from the previous U (row y1B, x2 = x2b .. x2b+3)
+        float S[4];
+        bool empty[4];
+        bool exact = exact_all;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            empty[j] = false;
+            S[j] = 0.f;
+            if (!exact && rvalid) {
+                const float u = L.Ut[(x2b + j) * d.pU + y1B].x;
+                if (u == -INFINITY) empty[j] = true;
+                else if (fabsf(u) < 1e30f) S[j] = u;
+                else exact = true;
+            }
+        }
+        if (!exact_all) exact = __any_sync(0xffffffffu, exact);
+        float acc[4];
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            if (exact) {
+                float Mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+                for (int c0 = 0; c0 < d.bc; c0 += 32) {
+                    phaseA(c0);
+                    __syncwarp();
+                    phaseB(c0, true, S, Mx);
+                    __syncwarp();
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    for (int o = YS >> 1; o > 0; o >>= 1) Mx[j] = fmaxf(Mx[j], __shfl_xor_sync(0xffffffffu, Mx[j], o));
+                    empty[j] = !(Mx[j] > -INFINITY);
+                    S[j] = empty[j] ? 0.f : Mx[j];
+                }
+            }
+            acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+            for (int c0 = 0; c0 < d.bc; c0 += 32) {
+                phaseA(c0);
+                __syncwarp();
+                phaseB(c0, false, S, acc);
+                __syncwarp();
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                for (int o = YS >> 1; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+            if (exact) break;
+            bool ok = true;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                ok = ok && (!rvalid || (empty[j] ? acc[j] == 0.f : (acc[j] >= 0.25f && acc[j] <= 4.0f)));
+            if (__all_sync(0xffffffffu, ok)) break;
+            exact = true;
+            if (lane == 0) ++fallbacks;
+        }
+        if (hB == 0 && rvalid) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                float2 u = make_float2(-INFINITY, 0.f);
+                if (!empty[j] && acc[j] > 1e-37f) {
+                    float lh, ll;
+                    ln_split(acc[j], gq, lh, ll);
+                    u = make_float2(S[j] + lh, ll);
+                    if (!(fabsf(u.x) < 1e30f)) nonfinite = 1;
+                }
+                L.Ut[(x2b + j) * d.pU + y1B] = u;
+            }
+        }
+    }
+}
+
+template <int NT, int AR, int NQ>
+__device__ __forceinline__ void fused_rg(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all,
+                                         const float2* LNUg, int& fb, int& nf) {
+    // row-group size: fewer idle warps in the last round vs. T-column reuse
+    const int nw = NT / 32;
+    const int r8 = ((d.br + 7) / 8 + nw - 1) / nw * 8;
+    const int r4 = ((d.br + 3) / 4 + nw - 1) / nw * 4;
+    if (8 * r4 < 7 * r8) fused_y2x1<NT, AR, NQ, 4>(L, d, gq, exact_all, LNUg, fb, nf);
+    else fused_y2x1<NT, AR, NQ, 8>(L, d, gq, exact_all, LNUg, fb, nf);
+}
+
 template <int NT>
-__device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base) {
-    const K1Lay L = k1_carve(base, p.s, p.bcap);
+__device__ void fused_dispatch(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all,
+                               const float2* LNUg, int& fb, int& nf) {
+    const int nq = d.ac / 4;
+    if (d.ar > 8) {
+        if (nq == 4) fused_rg<NT, 16, 4>(L, d, gq, exact_all, LNUg, fb, nf);
+        else if (nq == 2) fused_rg<NT, 16, 2>(L, d, gq, exact_all, LNUg, fb, nf);
+        else fused_rg<NT, 16, 1>(L, d, gq, exact_all, LNUg, fb, nf);
+    } else {
+        if (nq == 4) fused_rg<NT, 8, 4>(L, d, gq, exact_all, LNUg, fb, nf);
+        else if (nq == 2) fused_rg<NT, 8, 2>(L, d, gq, exact_all, LNUg, fb, nf);
+        else fused_rg<NT, 8, 1>(L, d, gq, exact_all, LNUg, fb, nf);
+    }
+}
+
+// BIG: the extraction's exact Y-iteration partial sums per basic-cell
+// quadrant (x1 half, x2 half via the split weights W[y2][x1] of PY1S),
+// one output y per thread, written to the global ACC slice.
+template <int NT>
+__device__ void final_split_big(const K1Lay& L, const Dims& d, float4* __restrict__ ACCg) {
+    const int ny = d.br * d.bc;
+    const int ks = min(d.s, d.ar);
+    for (int y = threadIdx.x; y < ny; y += NT) {
+        const int y1 = y / d.bc, y2 = y % d.bc;
+        const float2* Tc = L.Tt + y2 * d.pT;
+        const float2* Wc = L.Ut + y2 * d.pT;
+        const float* ctp = L.CT + d.off - y1;      // C(x1 - y1) = ctp[x1]
+        float M = -INFINITY;
+        for (int x = 0; x < d.ar; ++x) M = fmaxf(M, Tc[x].x - ctp[x]);
+        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (M > -INFINITY) {
+            for (int x = 0; x < d.ar; ++x) {
+                const float2 t = Tc[x];
+                const float e = ex2f(((t.x - ctp[x]) - M) * kL2E + t.y);
+                const float2 w = Wc[x];
+                if (x < ks) { q.x = fmaf(e, w.x, q.x); q.y = fmaf(e, w.y, q.y); }
+                else { q.z = fmaf(e, w.x, q.z); q.w = fmaf(e, w.y, q.w); }
+            }
+        }
+        ACCg[y] = q;
+    }
+}
+
+// ----------------------------------------------------------- the solve --
+template <int NT, bool BIG>
+__device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, unsigned char* gslice) {
+    const K1Lay L = k1_carve(base, p.s, p.bcap, BIG, NT / 32);
     __shared__ int4 s_box[4];
     __shared__ long long s_off[4];
     __shared__ int s_q[4];          // quadrant of each member
@@ -432,7 +688,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base) 
     co.iters = 0; co.flags = 0; co.err = 0.f; co.box = max(d.br, d.bc); co.mufu = 0.0;
     co.fallbacks = 0; co.pad = 0;
 
-    if (d.br > p.bcap || d.bc > p.bcap || d.br == 0) {
+    if (d.br > p.bcap || d.bc > p.bcap || d.br == 0 || (BIG && (d.ac % 4 != 0 || d.ar > 16 || d.ac > 16))) {
         if (tid == 0) {
             co.flags = 2;   // misrouted (tier classification) or empty support
             atomicOr(p.overflow, 2);
@@ -496,6 +752,10 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base) 
         L.MU[x] = (float)m;
     }
     // ---- line 8: nu_cell = sum_i nu_i on the union box; log nu_cell
+    // (BIG: log nu_cell and the extraction sums live in the CTA's global slice)
+    float2* LNU = BIG ? reinterpret_cast<float2*>(gslice) : L.LNU;
+    float4* ACCp = BIG ? reinterpret_cast<float4*>(gslice + (((size_t)p.bcap * p.bcap * sizeof(float2) + 255) & ~(size_t)255))
+                       : reinterpret_cast<float4*>(L.G);
     const int ny = d.br * d.bc;
     double npos = 0.0;
     for (int y = tid; y < ny; y += NT) {
@@ -506,7 +766,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base) 
             const int ry = gy - b.x, rx = gx - b.y;
             if (ry >= 0 && ry < b.z && rx >= 0 && rx < b.w) v += p.pool_in[s_off[m] + (long long)ry * b.w + rx];
         }
-        L.LNU[y] = (v > 0.0) ? split_hl(log(v), gq) : make_float2(-INFINITY, 0.f);
+        LNU[y] = (v > 0.0) ? split_hl(log(v), gq) : make_float2(-INFINITY, 0.f);
         npos += (v > 0.0) ? 1.0 : 0.0;
     }
     npos = block_sum(npos, L.red);     // (barrier: staging complete)
@@ -522,9 +782,13 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base) 
         double e_loc = 0.0;
         lse_pass<PY1, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
         __syncthreads();
-        lse_pass<PY2, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
-        __syncthreads();
-        lse_pass<PX1, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
+        if (BIG) {
+            fused_dispatch<NT>(L, d, gq, exact, LNU, fallbacks, nonfinite);
+        } else {
+            lse_pass<PY2, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
+            __syncthreads();
+            lse_pass<PX1, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
+        }
         __syncthreads();
         lse_pass<PX2, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
         err = block_sum(e_loc, L.red);      // includes the barrier
@@ -539,7 +803,8 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base) 
         double dummy = 0.0;
         lse_pass<PY1S, NT>(L, d, gq, true, Fc, Fn, dummy, fallbacks, nonfinite);
         __syncthreads();
-        lse_pass<PY2S, NT>(L, d, gq, true, Fc, Fn, dummy, fallbacks, nonfinite);
+        if (BIG) final_split_big<NT>(L, d, ACCp);
+        else lse_pass<PY2S, NT>(L, d, gq, true, Fc, Fn, dummy, fallbacks, nonfinite);
     }
     if (nonfinite) atomicOr(&s_flag, 2);
     fallbacks = (int)block_sum((double)fallbacks, L.red + 32);
@@ -557,7 +822,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base) 
     }
 
     // ---- epilogue (ACC over the G+LNU region; nu_cell re-gathered from pool_in)
-    const float4* ACC = reinterpret_cast<const float4*>(L.G);
+    const float4* ACC = ACCp;
     auto nucell = [&](int y) {
         const int gy = Y0 + y / d.bc, gx = X0 + y % d.bc;
         double v = 0.0;
@@ -702,11 +967,14 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base) 
 }
 
 // Persistent CTAs pulling cells from a tier list (K0 classification).
-template <int NT, bool GMEM>
-__global__ void __launch_bounds__(NT, (NT == 256 ? 3 : 1)) k1_cell_solve(SweepParams p) {
+// BIG = false: all per-cell arrays in SMEM (small Y boxes, 3 CTAs/SM);
+// BIG = true: fused Y2+X1 path, O(a b) SMEM + a global slice per CTA.
+template <int NT, bool BIG, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k1_cell_solve(SweepParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_cell;
-    unsigned char* base = GMEM ? p.gscratch + (long long)blockIdx.x * p.gslice : smem;
+    unsigned char* base = smem;
+    unsigned char* gslice = BIG ? p.gscratch + (long long)blockIdx.x * p.gslice : nullptr;
     while (true) {
         if (threadIdx.x == 0) {
             const int k = atomicAdd(p.work_counter, 1);
@@ -715,13 +983,16 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 3 : 1)) k1_cell_solve(SweepPa
         __syncthreads();
         const int cell = s_cell;
         if (cell < 0) return;
-        solve_cell<NT>(p, cell, base);
+        solve_cell<NT, BIG>(p, cell, base, gslice);
         __syncthreads();
     }
 }
 
-// K0: route every cell of the sweep to a tier by its union Y-box side.
-__global__ void k0_classify(SweepParams p, int b0, int b1, int* lists, int* counts, int ncap) {
+// K0: route every cell of the sweep to a tier by its union Y-box side
+// (tier 0 <= b0: SMEM path; tier 1 <= b1 and tier 2 (beyond): BIG path;
+// cells beyond tier 2's capacity are flagged by the solve), and record the
+// side for the LPT ordering of the big tiers.
+__global__ void k0_classify(SweepParams p, int b0, int b1, int* lists, int* counts, int ncap, int* bside) {
     const int cell = blockIdx.x * blockDim.x + threadIdx.x;
     if (cell >= p.ncells) return;
     const int cp = cell / p.nca, cq = cell % p.nca;
@@ -737,37 +1008,66 @@ __global__ void k0_classify(SweepParams p, int b0, int b1, int* lists, int* coun
             y1 = max(y1, b.x + b.z - 1); x1 = max(x1, b.y + b.w - 1);
         }
     const int bmax = y1 >= 0 ? max(y1 - y0 + 1, x1 - x0 + 1) : 0;
-    const int tier = bmax <= b0 ? 0 : (bmax <= b1 ? 1 : 2);
+    const bool small_x = p.s < 4;       // the BIG path needs a_c % 4 == 0
+    const int tier = (bmax <= b0 || small_x) ? 0 : (bmax <= b1 ? 1 : 2);
     const int k = atomicAdd(&counts[tier], 1);
     lists[tier * ncap + k] = cell;
+    bside[cell] = bmax;
 }
 
-size_t k1_smem_bytes_host(int s, int bcap) { return k1_smem_bytes(s, bcap); }
+// LPT order for the big tiers: counting sort of the tier-t list by box side,
+// descending (largest, slowest cells start first).  One block per tier.
+__global__ void k0_sort(const int* lists, const int* counts, int ncap, const int* bside, int* sorted) {
+    __shared__ int hist[1024];
+    const int t = 1 + blockIdx.x;
+    const int n = counts[t];
+    const int* in = lists + (size_t)t * ncap;
+    int* out = sorted + (size_t)blockIdx.x * ncap;
+    for (int k = threadIdx.x; k < 1024; k += blockDim.x) hist[k] = 0;
+    __syncthreads();
+    for (int k = threadIdx.x; k < n; k += blockDim.x) atomicAdd(&hist[1023 - min(bside[in[k]], 1023)], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int k = 0; k < 1024; ++k) { const int v = hist[k]; hist[k] = acc; acc += v; }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const int c = in[k];
+        out[atomicAdd(&hist[1023 - min(bside[c], 1023)], 1)] = c;
+    }
+}
 
-cudaError_t launch_k0(const SweepParams& p, int b0, int b1, int* lists, int* counts, int ncap, cudaStream_t st) {
-    k0_classify<<<(p.ncells + 255) / 256, 256, 0, st>>>(p, b0, b1, lists, counts, ncap);
+size_t k1_smem_bytes_host(int s, int bcap, bool big, int nwarps) { return k1_smem_bytes(s, bcap, big, nwarps); }
+
+cudaError_t launch_k0(const SweepParams& p, int b0, int b1, int* lists, int* counts, int ncap, int* bside,
+                      int* sorted, cudaStream_t st) {
+    k0_classify<<<(p.ncells + 255) / 256, 256, 0, st>>>(p, b0, b1, lists, counts, ncap, bside);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k0_sort<<<2, 1024, 0, st>>>(lists, counts, ncap, bside, sorted);
     return cudaGetLastError();
 }
 
-template <int NT, bool GMEM>
+template <int NT, bool BIG, int MINB>
 static cudaError_t launch_tier(const SweepParams& p, int grid, size_t smem, cudaStream_t st) {
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
-        cudaError_t e = cudaFuncSetAttribute(k1_cell_solve<NT, GMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(k1_cell_solve<NT, BIG, MINB>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr = smem;
     }
-    k1_cell_solve<NT, GMEM><<<grid, NT, smem, st>>>(p);
+    k1_cell_solve<NT, BIG, MINB><<<grid, NT, smem, st>>>(p);
     return cudaGetLastError();
 }
 
-// tier 0: 256 threads, several CTAs per SM; tier 1: 512 threads, large SMEM;
-// tier 2: 512 threads with the cell's arrays in an L2-resident global slice.
+// tier 0: 256 threads, all arrays in SMEM, 3 CTAs/SM;
+// tier 1: BIG path, 256 threads, 2 CTAs/SM; tier 2: BIG path, 512 threads, 1 CTA/SM.
 cudaError_t launch_k1(const SweepParams& p, int tier, int grid, size_t smem, cudaStream_t st) {
-    if (tier == 0) return launch_tier<256, false>(p, grid, smem, st);
-    if (tier == 1) return launch_tier<512, false>(p, grid, smem, st);
-    return launch_tier<512, true>(p, grid, 0, st);
+    if (tier == 0) return launch_tier<256, false, 3>(p, grid, smem, st);
+    if (tier == 1) return launch_tier<256, true, 2>(p, grid, smem, st);
+    return launch_tier<512, true, 1>(p, grid, smem, st);
 }
 
 }  // namespace dd

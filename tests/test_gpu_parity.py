@@ -169,3 +169,52 @@ def test_validation_errors_gpu(DD):
         DD(mu, mu * 1.01, 1.0, 4)
     with pytest.raises(ValueError):
         DD(mu, mu, 1.0, 16)
+
+
+@pytest.mark.parametrize("bcap_main,bcap_big", [(10, 0), (10, 12)])
+def test_big_tier_parity_cfg1(DD, bcap_main, bcap_big):
+    """The fused Y2+X1 path (K1 tiers 1 and 2) vs the oracle: routing every
+    cell with a union Y box > 10 px away from the SMEM tier (and, with
+    bcap_big = 12, everything beyond 12 px to the 512-thread tier)."""
+    mu, nu = config_images(1)
+    eps = 2.0 / 32**2
+    g = DD(mu, nu, eps, 4, err_tol=1e-6, bcap_main=bcap_main, bcap_big=bcap_big)
+    o = Oracle(mu, nu, eps, 4, err_tol=1e-6)
+    mass = _mass_i(mu, 4)
+    for sweep in range(2):
+        g.iterate(1)
+        o.iterate(1)
+        Dg, Do = g.basic_marginals_dense(), o.basic_marginals_dense()
+        diff = np.abs(Dg - Do).sum(1)
+        assert (diff <= 4e-6 * np.maximum(mass, 1e-3)).all(), (sweep, diff.max())
+        assert np.abs(Dg.sum(0) - nu.ravel()).sum() < 1e-11
+        np.testing.assert_allclose(Dg.sum(1), mass, rtol=1e-10, atol=1e-12)
+    g.iterate(10)
+    o.iterate(10)
+    assert g.totals()["big_cells"] > 0
+    cg, _ = g.primal_cost()
+    co, _ = o.primal_cost()
+    assert abs(cg - co) <= 1e-5 * co, (cg, co)
+    lx, ly = g.marginal_error()
+    assert lx <= 1e-6 and ly <= 1e-6, (lx, ly)
+
+
+@pytest.mark.parametrize("bcap_big", [0, 40])
+def test_big_tier_parity_s8(DD, bcap_big):
+    """s = 8 composite cells (16 x 16 X boxes, 16 x 8 edges, 8 x 8 corners) on
+    the fused path: 32^2, kappa = 0.5, all cells off the SMEM tier."""
+    n, s = 32, 8
+    mu, nu = gaussian_mixture_image(n, 11, 3), gaussian_mixture_image(n, 12, 3)
+    eps = 0.5 / n**2
+    g = DD(mu, nu, eps, s, err_tol=1e-6, bcap_main=18, bcap_big=bcap_big)
+    o = Oracle(mu, nu, eps, s, err_tol=1e-6)
+    g.iterate(6)
+    o.iterate(6)
+    assert g.totals()["big_cells"] > 0
+    cg, _ = g.primal_cost()
+    co, _ = o.primal_cost()
+    assert abs(cg - co) <= 1e-5 * co, (cg, co)
+    lx, ly = g.marginal_error()
+    assert lx <= 1e-6 and ly <= 1e-6, (lx, ly)
+    Dg, Do = g.basic_marginals_dense(), o.basic_marginals_dense()
+    assert np.abs(Dg - Do).sum() <= 1e-5

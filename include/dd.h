@@ -160,10 +160,10 @@ int dd_reset_totals(dd_ctx* ctx);
 
 /* dd_get_cell_stats -- per composite cell of the last sweep (cell index =
  * row-major over the partition's cell grid): Sinkhorn iterations, union
- * Y-box side max(b_r, b_c) and MUFU ops of the solve.  Any output may be
- * NULL.  Returns the number of cells (<= max_cells are written), or < 0 on
- * error (-DD_E*). */
-int dd_get_cell_stats(dd_ctx* ctx, int* iters, int* box_side, double* mufu_ops, int max_cells);
+ * Y-box side max(b_r, b_c), MUFU ops of the solve and its duration on its SM
+ * in units of 1024 cycles.  Any output may be NULL.  Returns the number of
+ * cells (<= max_cells are written), or < 0 on error (-DD_E*). */
+int dd_get_cell_stats(dd_ctx* ctx, int* iters, int* box_side, double* mufu_ops, int* kcycles, int max_cells);
 
 /* State export/import for single-sweep parity.  Layout as in
  * DD_PLAN_BASIC_MARGINALS plus alpha_A, alpha_B (side*side fp64, cost units).

@@ -25,7 +25,7 @@ struct CellOut {
     int box;          // max(b_r, b_c) of the union Y box
     double mufu;      // MUFU ops executed (ex2 + lg2/rcp), without fallbacks
     int fallbacks;    // outputs recomputed with an exact max (speculative miss)
-    int pad;
+    int pad;          // solve time of the cell in units of 1024 SM cycles (diagnostic)
 };
 
 struct SweepParams {
@@ -64,6 +64,11 @@ struct SweepParams {
 __device__ __forceinline__ float ex2f(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float lg2f(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
 __device__ __forceinline__ float fmax3f(float a, float b, float c) {   // FMNMX3 (sm_100)

@@ -188,7 +188,7 @@ int check_overflow(dd_ctx* c) {
 //   tier 0 (SMEM path, 256 threads, 3 CTAs/SM): union Y box <= bcap_main;
 //   tier 1 (BIG path, 256 threads, 2 CTAs/SM): <= bcap_big (<= kCap1);
 //   tier 2 (BIG path, 512 threads, 1 CTA/SM):  <= bcap_big2 (<= kCap2).
-constexpr int kCap1 = 320, kCap2 = 704;
+constexpr int kCap1 = 120, kCap2 = 704;   // tier-1 cap 120: measured best split
 constexpr size_t kSmem1 = 110 * 1024, kSmem2 = 220 * 1024;
 void tier_caps(int s, int opt_main, int opt_big, int* b0, int* b1, int* b2) {
     int want = (s <= 4) ? 32 : 40;
@@ -580,7 +580,7 @@ int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, d
     CK(cudaMalloc(&c->counters, 8 * sizeof(int)));
     CK(cudaMemsetAsync(c->counters, 0, 8 * sizeof(int), c->st));
     // BIG tiers: one global slice per persistent CTA holding log nu_cell
-    // (b^2 float2) and the extraction partial sums (b^2 float4), sized for
+    // (b^2 float2), the phase-A stabilisers (b^2 float) and the extraction partial sums (b^2 float4), sized for
     // the largest tier capacity over the layers (box sides never exceed the side)
     for (int k = 0; k < nl; ++k) {
         int b0, b1, b2;
@@ -592,7 +592,9 @@ int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, d
     c->grid_t[1] = prop.multiProcessorCount;
     for (int t = 0; t < 2; ++t) {
         const long long b = c->slice_cap[t];
-        c->slice_bytes[t] = (((b * b * (long long)sizeof(float2) + 255) & ~255LL) + b * b * (long long)sizeof(float4) + 255) & ~255LL;
+        auto al = [](long long v) { return (v + 255) & ~255LL; };
+        c->slice_bytes[t] = al(b * b * (long long)sizeof(float2)) + al(b * b * (long long)sizeof(float)) +
+                            al(b * b * (long long)sizeof(float4));
         CK(cudaMalloc(&c->slices[t], (size_t)c->slice_bytes[t] * c->grid_t[t]));
     }
     for (int k = 0; k < 2; ++k) {
@@ -722,7 +724,7 @@ int dd_get_totals(dd_ctx* c, dd_sweep_stats* s) {
     return DD_OK;
 }
 
-int dd_get_cell_stats(dd_ctx* c, int* iters, int* box_side, double* mufu_ops, int max_cells) {
+int dd_get_cell_stats(dd_ctx* c, int* iters, int* box_side, double* mufu_ops, int* kcycles, int max_cells) {
     if (!c || max_cells < 0) return -DD_EINVAL;
     int rc = harvest(c);
     if (rc) return -rc;
@@ -741,6 +743,7 @@ int dd_get_cell_stats(dd_ctx* c, int* iters, int* box_side, double* mufu_ops, in
             if (iters) iters[k] = h[k].iters;
             if (box_side) box_side[k] = h[k].box;
             if (mufu_ops) mufu_ops[k] = h[k].mufu;
+            if (kcycles) kcycles[k] = h[k].pad;
         }
     }
     return ncells;

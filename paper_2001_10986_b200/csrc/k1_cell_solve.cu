@@ -43,6 +43,7 @@ struct K1Lay {
     float* CT;    // cost table C(d) = d^2 / kappa, d in [-OFF, OFF]
     double* red;  // reduction scratch (64)
     float2* gbuf; // BIG: per-warp G rows of the fused Y2+X1 pass [warp][kGbufPerWarp]
+    float2* CP;   // BIG: cost pairs CP[k] = (CT[k], CT[k-1])
 };
 
 // BIG mode (fused Y2+X1): G is never stored as
@@ -66,17 +67,18 @@ __host__ __device__ inline void k1_sizes(int s, int bcap, size_t* sz, bool big =
     sz[8] = align16((2 * k1_ct_off(s, bcap) + 8) * 4);  // CT
     sz[9] = 64 * 8;                                     // red
     sz[10] = big ? (size_t)nwarps * kGbufPerWarp * 8 : 0;   // gbuf
+    sz[11] = big ? align16((2 * k1_ct_off(s, bcap) + 8) * 8) : 0;   // CP
 }
 
 __host__ __device__ inline size_t k1_smem_bytes(int s, int bcap, bool big = false, int nwarps = 0) {
-    size_t sz[11], b = 0;
+    size_t sz[12], b = 0;
     k1_sizes(s, bcap, sz, big, nwarps);
-    for (int k = 0; k < 11; ++k) b += sz[k];
+    for (int k = 0; k < 12; ++k) b += sz[k];
     return b;
 }
 
 __device__ inline K1Lay k1_carve(unsigned char* base, int s, int bcap, bool big = false, int nwarps = 0) {
-    size_t sz[11];
+    size_t sz[12];
     k1_sizes(s, bcap, sz, big, nwarps);
     K1Lay L;
     size_t o = 0;
@@ -90,7 +92,8 @@ __device__ inline K1Lay k1_carve(unsigned char* base, int s, int bcap, bool big 
     L.LNU = (float2*)(base + o); o += sz[7];
     L.CT = (float*)(base + o);   o += sz[8];
     L.red = (double*)(base + o); o += sz[9];
-    L.gbuf = (float2*)(base + o);
+    L.gbuf = (float2*)(base + o); o += sz[10];
+    L.CP = (float2*)(base + o);
     return L;
 }
 
@@ -390,25 +393,34 @@ __device__ __forceinline__ void lse_pass(const K1Lay& L, const Dims& d, const Gr
 }
 
 // ------------------------------------------------- BIG: fused Y2 + X1 pass --
-// For every Y row y1 (row groups of RG rows per warp, no block barrier):
+// For every Y row y1 (row groups of RG = 8 rows per warp, no block barrier):
 //   phase A (lane <-> y2 of a 32-column chunk):
 //     G(y1, y2) = log nu_cell(y1, y2) - LSE_x1[T(x1, y2) - C(x1 - y1)]
-//     (exact max over the AR terms held in registers; the T column is reused
-//     by the RG rows of the group)
+//     with the speculative stabiliser S = this output's LSE of the previous
+//     iteration (global slice SL, on the hi grid); rows are processed in
+//     pairs so that one packed FADD2/FFMA2 serves two exps with T(x1, y2)
+//     broadcast and the cost pair (C(x1-y1), C(x1-y1-1)) one LDS.64 from the
+//     pair table CP; an output whose sum leaves [1/4, 4] is recomputed with
+//     an exact max (first iteration: exact two-pass for all).
 //   phase B (lane <-> (row r, x2 quad, y2 sub-slice)):
 //     U(y1, x2) += sum_{y2 in chunk} exp(G(y1, y2) - C(y2 - x2) - S(y1, x2))
-//     (speculative stabiliser S = previous U, sliding cost window; exact
-//     two-pass max on the first iteration or when the window check fails)
+//     (S = previous U; cost pairs slide with period 2 over y2; exact two-pass
+//     max on the first iteration or when the window check fails).
 // G lives only in a per-warp buffer of one chunk; U is written to Ut[x2][y1]
 // for the X2 pass.  Algorithmic exps: ar br bc (phase A) + br bc ac (phase B)
 // = the Y2 and X1 passes of the separable scheme.
-template <int NT, int AR, int NQ, int RG>
+constexpr int kRG = 4;
+
+__device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
+
+template <int NT, int AR, int NQ>
 __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all,
-                                           const float2* __restrict__ LNUg, int& fallbacks, int& nonfinite) {
+                                           const float2* __restrict__ LNUg, float* __restrict__ SLg,
+                                           int& fallbacks, int& nonfinite) {
+    constexpr int RG = kRG;
     constexpr int YS = 32 / (RG * NQ);      // phase-B lanes sharing one output (y2 split)
     constexpr int SUB = 32 / YS;            // y2 per phase-B lane slice of a chunk
     constexpr int PR = YS * (SUB + 1);      // gbuf row pitch (float2), conflict-free
-    constexpr int NWA = AR + RG - 1;        // phase-A cost window
     static_assert(RG * PR <= kGbufPerWarp, "gbuf");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float2* gb = L.gbuf + warp * kGbufPerWarp;
@@ -417,62 +429,104 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
     const int qB = (lane / YS) % NQ;
     const int hB = lane % YS;
     const int x2b = 4 * qB;
+    const bool qvalid = x2b < d.ac;       // NQ = 4 serves a_c = 16; NQ = 2 serves a_c = 8 and 4
     const int gidxA = (lane / SUB) * (SUB + 1) + lane % SUB;   // phase-A write slot of this lane's y2
     const float2 L2E2 = make_float2(kL2E, kL2E);
+    const float2* CP = L.CP;
 
     for (int grp = warp; grp < ngroups; grp += NT / 32) {
         const int y1b = grp * RG;
         const int y1B = y1b + rB;
         const bool rvalid = y1B < d.br;
-        // phase-A cost window: C(x1 - (y1b + r)) = wA[x1 - r + RG - 1]
-        float wA[NWA];
-        {
-            const float* cw = L.CT + d.off - y1b - (RG - 1);
-#pragma unroll
-            for (int m = 0; m < NWA; ++m) wA[m] = cw[m];
-        }
+        const int cpo = d.off - y1b;        // CP[cpo + x - r] = (C(x - y1b - r), C(x - y1b - r - 1))
+
+        // ---------------------------------------------------------- phase A
         auto phaseA = [&](int c0) {
             const int y2 = c0 + lane;
             const bool vy = y2 < d.bc;
-            float th[AR], tl[AR];
-#pragma unroll
-            for (int x = 0; x < AR; ++x) {
-                const float2 t = (vy && x < d.ar) ? L.Tt[y2 * d.pT + x] : make_float2(-INFINITY, 0.f);
-                th[x] = t.x;
-                tl[x] = t.y;
-            }
+            const int y2c = vy ? y2 : d.bc - 1;          // clamped: every lane runs the same code
             float2 ln[RG];
+            float sp[RG];
 #pragma unroll
-            for (int r = 0; r < RG; ++r)
-                ln[r] = (vy && y1b + r < d.br) ? LNUg[(y1b + r) * d.bc + y2] : make_float2(-INFINITY, 0.f);
+            for (int r = 0; r < RG; ++r) {
+                const bool v = vy && (y1b + r < d.br);
+                const int idx = (y1b + r) * d.bc + y2;
+                ln[r] = v ? LNUg[idx] : make_float2(-INFINITY, 0.f);
+                sp[r] = v ? SLg[idx] : 0.f;
+            }
+            const float2* __restrict__ Tc = L.Tt + y2c * d.pT;
+            const float2* __restrict__ cpb = CP + cpo;     // cpb[x - r] = (C(x-y1b-r), C(x-y1b-r-1))
+            if (exact_all) {
+                // exact two-pass: stabiliser = max_x1 (T.hi - C)
+                float2 M[RG / 2];
+#pragma unroll
+                for (int i = 0; i < RG / 2; ++i) M[i] = make_float2(-INFINITY, -INFINITY);
+#pragma unroll 4
+                for (int x = 0; x < AR; ++x) {
+                    float th = Tc[x].x;
+                    if (AR == 8) th = (x < d.ar) ? th : -INFINITY;
+#pragma unroll
+                    for (int i = 0; i < RG / 2; ++i) {
+                        const float2 tt = __fadd2_rn(make_float2(th, th), neg2(cpb[x - 2 * i]));
+                        M[i] = make_float2(fmaxf(M[i].x, tt.x), fmaxf(M[i].y, tt.y));
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < RG / 2; ++i) {
+                    sp[2 * i] = M[i].x > -INFINITY ? M[i].x : 0.f;
+                    sp[2 * i + 1] = M[i].y > -INFINITY ? M[i].y : 0.f;
+                }
+            }
+            float2 nS[RG / 2], acc[RG / 2];
+#pragma unroll
+            for (int i = 0; i < RG / 2; ++i) {
+                nS[i] = make_float2(-sp[2 * i], -sp[2 * i + 1]);
+                acc[i] = make_float2(0.f, 0.f);
+            }
+#pragma unroll 4
+            for (int x = 0; x < AR; ++x) {
+                float2 t = Tc[x];
+                if (AR == 8) t.x = (x < d.ar) ? t.x : -INFINITY;     // s = 4 edge cells (a_r = 4)
+#pragma unroll
+                for (int i = 0; i < RG / 2; ++i) {
+                    float2 tt = __fadd2_rn(make_float2(t.x, t.x), neg2(cpb[x - 2 * i]));
+                    tt = __fadd2_rn(tt, nS[i]);
+                    tt = __ffma2_rn(tt, L2E2, make_float2(t.y, t.y));
+                    acc[i] = __fadd2_rn(acc[i], make_float2(ex2f(tt.x), ex2f(tt.y)));
+                }
+            }
 #pragma unroll
             for (int r = 0; r < RG; ++r) {
                 float2 g = make_float2(-INFINITY, 0.f);
-                if (ln[r].x != -INFINITY) {
-                    float t[AR];
-#pragma unroll
-                    for (int x = 0; x < AR; x += 2) {
-                        const float2 tt = __fadd2_rn(make_float2(th[x], th[x + 1]),
-                                                     make_float2(-wA[x - r + RG - 1], -wA[x + 1 - r + RG - 1]));
-                        t[x] = tt.x;
-                        t[x + 1] = tt.y;
+                float s = (r & 1) ? acc[r >> 1].y : acc[r >> 1].x;
+                float S = sp[r];
+                const bool live = ln[r].x != -INFINITY;
+                // exact recompute of an output whose speculative window failed
+                // (warp-uniform loop; rare after the first iterations of a solve)
+                const bool bad = live && (exact_all ? !(s > 0.f) : !(s >= 0.25f && s <= 4.0f));
+                if (__any_sync(0xffffffffu, bad)) {
+                    if (bad) {
+                        float M = -INFINITY;
+                        for (int x = 0; x < d.ar; ++x) M = fmaxf(M, Tc[x].x - cpb[x - r].x);
+                        s = 0.f;
+                        if (M > -INFINITY)
+                            for (int x = 0; x < d.ar; ++x) {
+                                const float2 t = Tc[x];
+                                s += ex2f(((t.x - cpb[x - r].x) - M) * kL2E + t.y);
+                            }
+                        S = M;
+                        if (!exact_all) ++fallbacks;
                     }
-                    float M = t[0];
-#pragma unroll
-                    for (int x = 1; x + 1 < AR; x += 2) M = fmax3f(M, t[x], t[x + 1]);
-                    if (AR % 2 == 0) M = fmaxf(M, t[AR - 1]);
-                    if (M > -INFINITY) {
-                        float2 s2 = make_float2(0.f, 0.f);
-                        const float2 nM = make_float2(-M, -M);
-#pragma unroll
-                        for (int x = 0; x < AR; x += 2) {
-                            float2 a = __fadd2_rn(make_float2(t[x], t[x + 1]), nM);
-                            a = __ffma2_rn(a, L2E2, make_float2(tl[x], tl[x + 1]));
-                            s2 = __fadd2_rn(s2, make_float2(ex2f(a.x), ex2f(a.y)));
-                        }
-                        float lh, ll;
-                        ln_split(s2.x + s2.y, gq, lh, ll);
-                        g = make_float2(ln[r].x - (M + lh), ln[r].y - ll);
+                }
+                if (live) {
+                    if (s > 1e-37f && S > -INFINITY) {
+                        const float l2 = lg2f(s);
+                        const float lh = gridq(l2 * kLN2, gq);
+                        const float ll2 = fmaf(-lh, kL2E, l2);
+                        const float Sn = S + lh;
+                        SLg[(y1b + r) * d.bc + y2] = Sn;
+                        g = make_float2(ln[r].x - Sn, ln[r].y - ll2);
+                        if (!(fabsf(Sn) < 1e30f)) nonfinite = 1;
                     } else {
                         nonfinite = 1;       // nu_cell(y) > 0 unreachable from X
                     }
@@ -480,41 +534,64 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
                 gb[r * PR + gidxA] = g;
             }
         };
-        // phase B over one chunk: MAXMODE -> running max, else sums with S
+
+        // ---------------------------------------------------------- phase B
         auto phaseB = [&](int c0, bool maxmode, const float* S, float* A) {
             const int ybase = c0 + hB * SUB;
             const int nk = min(SUB, d.bc - ybase);
-            const float2* grow = gb + rB * PR + hB * (SUB + 1);
-            const float* ctp = L.CT + d.off + ybase - x2b;    // C(y2 - x2b - j) = ctp[k - j]
-            float c1 = ctp[-1], c2 = ctp[-2], c3 = ctp[-3];
+            const float2* __restrict__ gp = gb + rB * PR + hB * (SUB + 1);
+            // pair table: cp[k] = (C(y2 - x2b), C(y2 - x2b - 1)), y2 = ybase + k; cp[k - 2] the next two
+            const float2* __restrict__ cp = CP + d.off + ybase - x2b;
             if (maxmode) {
                 for (int k = 0; k < nk; ++k) {
-                    const float c0v = ctp[k];
-                    const float gx = grow[k].x;
-                    A[0] = fmaxf(A[0], gx - c0v); A[1] = fmaxf(A[1], gx - c1);
-                    A[2] = fmaxf(A[2], gx - c2); A[3] = fmaxf(A[3], gx - c3);
-                    c3 = c2; c2 = c1; c1 = c0v;
+                    const float gx = gp[k].x;
+                    const float2 p0 = cp[k], p1 = cp[k - 2];
+                    A[0] = fmaxf(A[0], gx - p0.x); A[1] = fmaxf(A[1], gx - p0.y);
+                    A[2] = fmaxf(A[2], gx - p1.x); A[3] = fmaxf(A[3], gx - p1.y);
                 }
-            } else {
-                const float2 nS01 = make_float2(-S[0], -S[1]), nS23 = make_float2(-S[2], -S[3]);
-                float2 a01 = make_float2(A[0], A[1]), a23 = make_float2(A[2], A[3]);
-#pragma unroll 2
-                for (int k = 0; k < nk; ++k) {
-                    const float c0v = ctp[k];
-                    const float2 g = grow[k];
-                    float2 t01 = __fadd2_rn(make_float2(g.x, g.x), make_float2(-c0v, -c1));
-                    float2 t23 = __fadd2_rn(make_float2(g.x, g.x), make_float2(-c2, -c3));
-                    t01 = __fadd2_rn(t01, nS01);
-                    t23 = __fadd2_rn(t23, nS23);
-                    t01 = __ffma2_rn(t01, L2E2, make_float2(g.y, g.y));
-                    t23 = __ffma2_rn(t23, L2E2, make_float2(g.y, g.y));
-                    a01 = __fadd2_rn(a01, make_float2(ex2f(t01.x), ex2f(t01.y)));
-                    a23 = __fadd2_rn(a23, make_float2(ex2f(t23.x), ex2f(t23.y)));
-                    c3 = c2; c2 = c1; c1 = c0v;
-                }
-                A[0] = a01.x; A[1] = a01.y; A[2] = a23.x; A[3] = a23.y;
+                return;
             }
+            const float2 nS01 = make_float2(-S[0], -S[1]), nS23 = make_float2(-S[2], -S[3]);
+            float2 a01 = make_float2(A[0], A[1]), a23 = make_float2(A[2], A[3]);
+            float2 b01 = make_float2(0.f, 0.f), b23 = make_float2(0.f, 0.f);   // second accumulator chain
+            auto body = [&](float2 g, float2 p01, float2 p23, float2& s01, float2& s23) {
+                float2 t01 = __fadd2_rn(make_float2(g.x, g.x), neg2(p01));
+                float2 t23 = __fadd2_rn(make_float2(g.x, g.x), neg2(p23));
+                t01 = __fadd2_rn(t01, nS01);
+                t23 = __fadd2_rn(t23, nS23);
+                t01 = __ffma2_rn(t01, L2E2, make_float2(g.y, g.y));
+                t23 = __ffma2_rn(t23, L2E2, make_float2(g.y, g.y));
+                s01 = __fadd2_rn(s01, make_float2(ex2f(t01.x), ex2f(t01.y)));
+                s23 = __fadd2_rn(s23, make_float2(ex2f(t23.x), ex2f(t23.y)));
+            };
+            // cost pairs slide with period 2: the (j=2,3) pair at k is the (j=0,1) pair at k-2
+            float2 pa = cp[-2], pb = cp[-1];
+            int k = 0;
+            for (; k + 4 <= nk; k += 4) {
+                const float2 p0 = cp[0], p1 = cp[1], p2 = cp[2], p3 = cp[3];
+                const float2 g0 = gp[0], g1 = gp[1], g2 = gp[2], g3 = gp[3];
+                body(g0, p0, pa, a01, a23);
+                body(g1, p1, pb, b01, b23);
+                body(g2, p2, p0, a01, a23);
+                body(g3, p3, p1, b01, b23);
+                pa = p2;
+                pb = p3;
+                gp += 4;
+                cp += 4;
+            }
+            for (; k < nk; ++k) {
+                const float2 p0 = cp[0];
+                body(gp[0], p0, pa, a01, a23);
+                pa = pb;
+                pb = p0;
+                ++gp;
+                ++cp;
+            }
+            a01 = __fadd2_rn(a01, b01);
+            a23 = __fadd2_rn(a23, b23);
+            A[0] = a01.x; A[1] = a01.y; A[2] = a23.x; A[3] = a23.y;
         };
+
         // speculative stabilisers from the previous U (row y1B, x2 = x2b .. x2b+3)
         float S[4];
         bool empty[4];
@@ -523,7 +600,7 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
         for (int j = 0; j < 4; ++j) {
             empty[j] = false;
             S[j] = 0.f;
-            if (!exact && rvalid) {
+            if (!exact && rvalid && qvalid) {
                 const float u = L.Ut[(x2b + j) * d.pU + y1B].x;
                 if (u == -INFINITY) empty[j] = true;
                 else if (fabsf(u) < 1e30f) S[j] = u;
@@ -531,43 +608,53 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
             }
         }
         if (!exact_all) exact = __any_sync(0xffffffffu, exact);
+        // passes: speculative -> one sum pass; exact -> max pass + sum pass.
+        // A failed speculative window check restarts the group in exact mode.
+        // (single call sites of phaseA / phaseB keep the code compact)
         float acc[4];
-        for (int attempt = 0; attempt < 2; ++attempt) {
-            if (exact) {
-                float Mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-                for (int c0 = 0; c0 < d.bc; c0 += 32) {
-                    phaseA(c0);
-                    __syncwarp();
-                    phaseB(c0, true, S, Mx);
-                    __syncwarp();
-                }
+        int pass = exact ? 0 : 1;          // 0: max pass, 1: sum pass
+        bool a_done = false;               // G of the (single) chunk still in gbuf
+        while (true) {
+            const bool maxmode = (pass == 0);
+            float A[4];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    for (int o = YS >> 1; o > 0; o >>= 1) Mx[j] = fmaxf(Mx[j], __shfl_xor_sync(0xffffffffu, Mx[j], o));
-                    empty[j] = !(Mx[j] > -INFINITY);
-                    S[j] = empty[j] ? 0.f : Mx[j];
-                }
-            }
-            acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+            for (int j = 0; j < 4; ++j) A[j] = maxmode ? -INFINITY : 0.f;
             for (int c0 = 0; c0 < d.bc; c0 += 32) {
-                phaseA(c0);
+                if (!a_done) phaseA(c0);
                 __syncwarp();
-                phaseB(c0, false, S, acc);
+                phaseB(c0, maxmode, S, A);
                 __syncwarp();
             }
+            a_done = (d.bc <= 32);
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-                for (int o = YS >> 1; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+                for (int o = YS >> 1; o > 0; o >>= 1) {
+                    const float v = __shfl_xor_sync(0xffffffffu, A[j], o);
+                    A[j] = maxmode ? fmaxf(A[j], v) : A[j] + v;
+                }
+            if (maxmode) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    empty[j] = !(A[j] > -INFINITY);
+                    S[j] = empty[j] ? 0.f : A[j];
+                }
+                exact = true;
+                pass = 1;
+                continue;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[j] = A[j];
             if (exact) break;
             bool ok = true;
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-                ok = ok && (!rvalid || (empty[j] ? acc[j] == 0.f : (acc[j] >= 0.25f && acc[j] <= 4.0f)));
+                ok = ok && (!rvalid || !qvalid ||
+                            (empty[j] ? acc[j] == 0.f : (acc[j] >= 0.25f && acc[j] <= 4.0f)));
             if (__all_sync(0xffffffffu, ok)) break;
-            exact = true;
             if (lane == 0) ++fallbacks;
+            pass = 0;
         }
-        if (hB == 0 && rvalid) {
+        if (hB == 0 && rvalid && qvalid) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 float2 u = make_float2(-INFINITY, 0.f);
@@ -580,32 +667,19 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
                 L.Ut[(x2b + j) * d.pU + y1B] = u;
             }
         }
+        __syncwarp();
     }
-}
-
-template <int NT, int AR, int NQ>
-__device__ __forceinline__ void fused_rg(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all,
-                                         const float2* LNUg, int& fb, int& nf) {
-    // row-group size: fewer idle warps in the last round vs. T-column reuse
-    const int nw = NT / 32;
-    const int r8 = ((d.br + 7) / 8 + nw - 1) / nw * 8;
-    const int r4 = ((d.br + 3) / 4 + nw - 1) / nw * 4;
-    if (8 * r4 < 7 * r8) fused_y2x1<NT, AR, NQ, 4>(L, d, gq, exact_all, LNUg, fb, nf);
-    else fused_y2x1<NT, AR, NQ, 8>(L, d, gq, exact_all, LNUg, fb, nf);
 }
 
 template <int NT>
 __device__ void fused_dispatch(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all,
-                               const float2* LNUg, int& fb, int& nf) {
-    const int nq = d.ac / 4;
+                               const float2* LNUg, float* SLg, int& fb, int& nf) {
     if (d.ar > 8) {
-        if (nq == 4) fused_rg<NT, 16, 4>(L, d, gq, exact_all, LNUg, fb, nf);
-        else if (nq == 2) fused_rg<NT, 16, 2>(L, d, gq, exact_all, LNUg, fb, nf);
-        else fused_rg<NT, 16, 1>(L, d, gq, exact_all, LNUg, fb, nf);
+        if (d.ac > 8) fused_y2x1<NT, 16, 4>(L, d, gq, exact_all, LNUg, SLg, fb, nf);
+        else fused_y2x1<NT, 16, 2>(L, d, gq, exact_all, LNUg, SLg, fb, nf);
     } else {
-        if (nq == 4) fused_rg<NT, 8, 4>(L, d, gq, exact_all, LNUg, fb, nf);
-        else if (nq == 2) fused_rg<NT, 8, 2>(L, d, gq, exact_all, LNUg, fb, nf);
-        else fused_rg<NT, 8, 1>(L, d, gq, exact_all, LNUg, fb, nf);
+        if (d.ac > 8) fused_y2x1<NT, 8, 4>(L, d, gq, exact_all, LNUg, SLg, fb, nf);
+        else fused_y2x1<NT, 8, 2>(L, d, gq, exact_all, LNUg, SLg, fb, nf);
     }
 }
 
@@ -687,7 +761,20 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     CellOut co;
     co.iters = 0; co.flags = 0; co.err = 0.f; co.box = max(d.br, d.bc); co.mufu = 0.0;
     co.fallbacks = 0; co.pad = 0;
+    const long long t_start = clock64();
 
+    // BIG: solve in the transposed frame when the box is wider than tall, so
+    // the fused Y2+X1 pass (parallel over Y rows) always runs over the longer
+    // side (warp balance).  Local (r, c) = global (c, r); the MUFU work is
+    // the same in both orientations.
+    const bool tr = BIG && (d.bc > d.br);
+    if (tr) {
+        const int t1 = d.ar; d.ar = d.ac; d.ac = t1;
+        const int t2 = d.br; d.br = d.bc; d.bc = t2;
+    }
+    // local <-> global offsets inside the X and Y boxes
+    auto goff = [tr](int r, int c, int& gr, int& gc) { if (tr) { gr = c; gc = r; } else { gr = r; gc = c; } };
+    auto qloc = [tr](int q) { return tr ? (((q & 1) << 1) | (q >> 1)) : q; };   // member quadrant, local frame
     if (d.br > p.bcap || d.bc > p.bcap || d.br == 0 || (BIG && (d.ac % 4 != 0 || d.ar > 16 || d.ac > 16))) {
         if (tid == 0) {
             co.flags = 2;   // misrouted (tier classification) or empty support
@@ -707,11 +794,18 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         const double dd = (double)(i - d.off);
         L.CT[i] = (float)(dd * dd * inv_kappa);
     }
+    if (BIG) {
+        for (int i = tid; i < 2 * d.off + 1; i += NT) {
+            const double a = (double)(i - d.off), b = (double)(i - 1 - d.off);
+            L.CP[i] = make_float2((float)(a * a * inv_kappa), (float)(b * b * inv_kappa));
+        }
+    }
     // ---- X side: F = alpha/eps + log mu - shift(x~) - lambda (local affine gauge)
     const int nx = d.ar * d.ac;
     double fmax_l = -INFINITY, fmin_l = INFINITY, muJ = 0.0;
     for (int x = tid; x < nx; x += NT) {
-        const int xr = x / d.ac, xc = x % d.ac;
+        int xr, xc;
+        goff(x / d.ac, x % d.ac, xr, xc);
         const long long g = (long long)(R0 + xr) * p.side + (C0 + xc);
         const double m = p.mu[g];
         muJ += m;
@@ -738,7 +832,8 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         gq.inv = ldexp(1.0, -q);
     }
     for (int x = tid; x < nx; x += NT) {
-        const int xr = x / d.ac, xc = x % d.ac;
+        int xr, xc;
+        goff(x / d.ac, x % d.ac, xr, xc);
         const long long g = (long long)(R0 + xr) * p.side + (C0 + xc);
         const double m = p.mu[g];
         float2 f = make_float2(-INFINITY, 0.f), lm = make_float2(-INFINITY, 0.f);
@@ -747,19 +842,25 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
             f = split_hl(p.alpha[g] * inv_eps + p.logmu[g] - sh - lambda, gq);
             lm = split_hl(p.logmu[g], gq);
         }
-        L.FX[xr * d.pX + xc] = f;
+        L.FX[(x / d.ac) * d.pX + x % d.ac] = f;
         L.LM[x] = lm;
         L.MU[x] = (float)m;
     }
     // ---- line 8: nu_cell = sum_i nu_i on the union box; log nu_cell
     // (BIG: log nu_cell and the extraction sums live in the CTA's global slice)
     float2* LNU = BIG ? reinterpret_cast<float2*>(gslice) : L.LNU;
-    float4* ACCp = BIG ? reinterpret_cast<float4*>(gslice + (((size_t)p.bcap * p.bcap * sizeof(float2) + 255) & ~(size_t)255))
+    const size_t b2 = (size_t)p.bcap * p.bcap;
+    float* SLg = BIG ? reinterpret_cast<float*>(gslice + ((b2 * sizeof(float2) + 255) & ~(size_t)255)) : nullptr;
+    float4* ACCp = BIG ? reinterpret_cast<float4*>(gslice + ((b2 * sizeof(float2) + 255) & ~(size_t)255) +
+                                                   ((b2 * sizeof(float) + 255) & ~(size_t)255))
                        : reinterpret_cast<float4*>(L.G);
     const int ny = d.br * d.bc;
     double npos = 0.0;
     for (int y = tid; y < ny; y += NT) {
-        const int gy = Y0 + y / d.bc, gx = X0 + y % d.bc;
+        int gy, gx;
+        goff(y / d.bc, y % d.bc, gy, gx);
+        gy += Y0;
+        gx += X0;
         double v = 0.0;
         for (int m = 0; m < nmem; ++m) {
             const int4 b = s_box[m];
@@ -783,7 +884,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         lse_pass<PY1, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
         __syncthreads();
         if (BIG) {
-            fused_dispatch<NT>(L, d, gq, exact, LNU, fallbacks, nonfinite);
+            fused_dispatch<NT>(L, d, gq, exact, LNU, SLg, fallbacks, nonfinite);
         } else {
             lse_pass<PY2, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
             __syncthreads();
@@ -824,7 +925,10 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     // ---- epilogue (ACC over the G+LNU region; nu_cell re-gathered from pool_in)
     const float4* ACC = ACCp;
     auto nucell = [&](int y) {
-        const int gy = Y0 + y / d.bc, gx = X0 + y % d.bc;
+        int gy, gx;
+        goff(y / d.bc, y % d.bc, gy, gx);
+        gy += Y0;
+        gx += X0;
         double v = 0.0;
         for (int m = 0; m < nmem; ++m) {
             const int4 b = s_box[m];
@@ -852,7 +956,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         const double qn[4] = {nrm0, nrm1, nrm2, nrm3};
         double dsum = 0.0, psum = 0.0, dmax = 0.0, dv[4] = {0, 0, 0, 0}, nm[4] = {1, 1, 1, 1};
         for (int m = 0; m < nmem; ++m) {
-            nm[m] = qn[s_q[m]];
+            nm[m] = qn[qloc(s_q[m])];
             dv[m] = nm[m] - p.mass_i[s_mem[m]];
             dmax = fmax(dmax, fabs(dv[m]));
             if (dv[m] > 0) dsum += dv[m]; else psum += -dv[m];
@@ -872,7 +976,8 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     __syncthreads();
     const double fd0 = s_bal[0], gr0 = s_bal[1], fd1 = s_bal[2], gr1 = s_bal[3];
     const double fd2 = s_bal[4], gr2 = s_bal[5], fd3 = s_bal[6], gr3 = s_bal[7];
-    const int q0 = s_q[0], q1 = nmem > 1 ? s_q[1] : 0, q2 = nmem > 2 ? s_q[2] : 0, q3 = nmem > 3 ? s_q[3] : 0;
+    const int q0 = qloc(s_q[0]), q1 = nmem > 1 ? qloc(s_q[1]) : 0, q2 = nmem > 2 ? qloc(s_q[2]) : 0,
+              q3 = nmem > 3 ? qloc(s_q[3]) : 0;
     auto pick = [](const float4& a, int qd) { return qd == 0 ? a.x : qd == 1 ? a.y : qd == 2 ? a.z : a.w; };
     // balanced value of member m at y
     auto balanced = [&](int y, int m) -> double {
@@ -896,7 +1001,8 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         for (int y = tid; y < ny; y += NT) {
             const double v = balanced(y, m);
             if (v >= p.tau && v > 0.0) {
-                const int yr = y / d.bc, yc = y % d.bc;
+                int yr, yc;
+                goff(y / d.bc, y % d.bc, yr, yc);
                 r0 = min(r0, yr); r1 = max(r1, yr); c0 = min(c0, yc); c1 = max(c1, yc);
             }
         }
@@ -939,7 +1045,8 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         const int r0 = nb4.x - Y0, c0 = nb4.y - X0;
         const int area = nb4.z * nb4.w;
         for (int k = tid; k < area; k += NT) {
-            const int y = (r0 + k / nb4.w) * d.bc + (c0 + k % nb4.w);
+            const int gr = r0 + k / nb4.w, gc = c0 + k % nb4.w;
+            const int y = tr ? gc * d.bc + gr : gr * d.bc + gc;
             const double val = balanced(y, m);
             p.scratch[o + k] = (val >= p.tau && val > 0.0) ? val : 0.0;
         }
@@ -950,9 +1057,10 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     }
     // store u_{C,J}: alpha = eps (F + lambda + shift - log mu)  (plan's F, A4)
     for (int x = tid; x < nx; x += NT) {
-        const int xr = x / d.ac, xc = x % d.ac;
+        int xr, xc;
+        goff(x / d.ac, x % d.ac, xr, xc);
         const long long g = (long long)(R0 + xr) * p.side + (C0 + xc);
-        const float2 f = Fc[xr * d.pX + xc];
+        const float2 f = Fc[(x / d.ac) * d.pX + x % d.ac];
         double a = 0.0;
         if (f.x > -INFINITY && p.mu[g] > 0.0) {
             const double sh = ((2.0 * xr + Dr) * Dr + (2.0 * xc + Dc) * Dc) * inv_kappa;
@@ -962,6 +1070,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     }
     if (tid == 0) {
         if (s_newoff[0] < 0) co.flags |= 8;
+        co.pad = (int)min((clock64() - t_start) >> 10, (long long)0x7fffffff);   // solve time, kcycles
         p.out[cell] = co;
     }
 }

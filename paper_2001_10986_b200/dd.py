@@ -74,7 +74,7 @@ def lib():
         L.dd_get_stats.argtypes = [p, C.POINTER(SweepStats)]
         L.dd_get_totals.argtypes = [p, C.POINTER(SweepStats)]
         L.dd_reset_totals.argtypes = [p]
-        L.dd_get_cell_stats.argtypes = [p, p, p, p, i]
+        L.dd_get_cell_stats.argtypes = [p, p, p, p, p, i]
         L.dd_get_state_info.argtypes = [p, C.POINTER(StateInfo)]
         L.dd_get_state.argtypes = [p, p, p, p, p, p]
         L.dd_set_state.argtypes = [p, i, ll, i, p, p, p, ll, p, p]
@@ -212,15 +212,16 @@ class DD:
         return self._check(lib().dd_reset_totals(self._h), "reset_totals")
 
     def cell_stats(self):
-        """Per composite cell of the last sweep: (iters, box_side, mufu_ops) arrays."""
-        n = lib().dd_get_cell_stats(self._h, None, None, None, 0)
+        """Per composite cell of the last sweep: (iters, box_side, mufu_ops, kcycles) arrays."""
+        n = lib().dd_get_cell_stats(self._h, None, None, None, None, 0)
         if n < 0:
             raise RuntimeError(f"dd_get_cell_stats rc={-n}: {self.last_error()}")
         it = np.zeros(max(n, 1), np.int32)
         bx = np.zeros(max(n, 1), np.int32)
         mf = np.zeros(max(n, 1), np.float64)
-        lib().dd_get_cell_stats(self._h, it.ctypes.data, bx.ctypes.data, mf.ctypes.data, n)
-        return it[:n], bx[:n], mf[:n]
+        kc = np.zeros(max(n, 1), np.int32)
+        lib().dd_get_cell_stats(self._h, it.ctypes.data, bx.ctypes.data, mf.ctypes.data, kc.ctypes.data, n)
+        return it[:n], bx[:n], mf[:n], kc[:n]
 
     def state_info(self):
         inf = StateInfo()

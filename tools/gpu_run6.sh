@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 300 python tools/profile_sweep.py --cfg 5 --profile-last --quiet > gpurun_out/plain6.log 2>&1 && \
+timeout 1500 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:k1_cell -o gpurun_out/k1_full_v3 -f python tools/profile_sweep.py --cfg 5 --profile-last --quiet > gpurun_out/ncu_full_v3.log 2>&1; echo ncu rc=$?
+tail -3 gpurun_out/ncu_full_v3.log

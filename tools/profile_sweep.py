@@ -24,6 +24,7 @@ ap.add_argument("--cfg", type=int, default=5)
 ap.add_argument("--profile-last", action="store_true")
 ap.add_argument("--quiet", action="store_true")
 ap.add_argument("--bcap", type=int, default=0)
+ap.add_argument("--bcap-big", type=int, default=0)
 ap.add_argument("--json", default="")
 ap.add_argument("--cells-npz", default="", help="dump per-cell (iters, box, mufu) of every sweep at side >= n/2")
 a = ap.parse_args()
@@ -31,7 +32,7 @@ p = CONFIGS[a.cfg]
 n, s = p["n"], p["s"]
 mu, nu = config_images(a.cfg)
 g = DD(mu, nu, p["kappa_final"] / n**2, s, schedule=SCHED_LADDER, coarsest_side=p.get("coarsest", 8),
-       eps_start=p.get("eps_start", 0.0), bcap_main=a.bcap)
+       eps_start=p.get("eps_start", 0.0), bcap_main=a.bcap, bcap_big=a.bcap_big)
 sched = build_schedule(n, p.get("coarsest", 8), p["kappa_final"], p.get("eps_start", 0.0))
 rows = []
 cell_dump = {}
@@ -54,8 +55,8 @@ for k, (side, kappa, sweeps) in enumerate(sched):
                                          "solve_ms", "big_cells", "max_box", "fallbacks", "mufu_ops")})
         rows.append(row)
         if a.cells_npz and side >= n // 2:
-            it, bx, mf = g.cell_stats()
-            cell_dump[f"s{side}_k{kappa}_j{j}"] = np.stack([it, bx, mf.astype(np.float64)])
+            it, bx, mf, kc = g.cell_stats()
+            cell_dump[f"s{side}_k{kappa}_j{j}"] = np.stack([it, bx, mf.astype(np.float64), kc])
         if not a.quiet:
             print(json.dumps(row), flush=True)
 tot = g.totals()

@@ -165,6 +165,14 @@ int dd_reset_totals(dd_ctx* ctx);
  * cells (<= max_cells are written), or < 0 on error (-DD_E*). */
 int dd_get_cell_stats(dd_ctx* ctx, int* iters, int* box_side, double* mufu_ops, int* kcycles, int max_cells);
 
+/* dd_phase_profile -- diagnostic: per-phase cycle counters of K1 summed over
+ * warps since the last call (32 uint64: [mode][16], mode 0 = SMEM tier,
+ * 1 = fused big-cell tiers; slots 0..5 = Y1 pass, barrier, Y2+X1, barrier,
+ * X2 pass, error reduction; 6 = Sinkhorn loop, 7 = prologue, 8 = epilogue,
+ * 9 = iterations).  All zero unless the library was built with
+ * -DDD_PHASE_PROF (tools/phase_profile.py).  Resets the counters. */
+int dd_phase_profile(dd_ctx* ctx, unsigned long long* out32);
+
 /* State export/import for single-sweep parity.  Layout as in
  * DD_PLAN_BASIC_MARGINALS plus alpha_A, alpha_B (side*side fp64, cost units).
  * Host buffers; values sized by dd_get_state_info().entries. */

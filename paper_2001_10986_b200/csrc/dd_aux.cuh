@@ -34,6 +34,7 @@ struct EvalParams {
     double* coo_m;
 };
 
+cudaError_t k1_phase_read(unsigned long long* out32);
 size_t k1_smem_bytes_host(int s, int bcap, bool big = false, int nwarps = 0);
 cudaError_t launch_k1(const SweepParams& p, int tier, int grid, size_t smem, cudaStream_t st);
 cudaError_t launch_k0(const SweepParams& p, int b0, int b1, int* lists, int* counts, int ncap, int* bside,

@@ -724,6 +724,14 @@ int dd_get_totals(dd_ctx* c, dd_sweep_stats* s) {
     return DD_OK;
 }
 
+int dd_phase_profile(dd_ctx* c, unsigned long long* out32) {
+    if (!c || !out32) return DD_EINVAL;
+    int rc = harvest(c);
+    if (rc) return rc;
+    CK(k1_phase_read(out32));
+    return DD_OK;
+}
+
 int dd_get_cell_stats(dd_ctx* c, int* iters, int* box_side, double* mufu_ops, int* kcycles, int max_cells) {
     if (!c || max_cells < 0) return -DD_EINVAL;
     int rc = harvest(c);

@@ -44,6 +44,9 @@ struct K1Lay {
     double* red;  // reduction scratch (64)
     float2* gbuf; // BIG: per-warp G rows of the fused Y2+X1 pass [warp][kGbufPerWarp]
     float2* CP;   // BIG: cost pairs CP[k] = (CT[k], CT[k-1])
+    float* XP;    // BIG: per-warp partial sums of the fused X2 LSE [warp][a_r a_c]
+    float* FH;    // BIG: F (current) as separate hi / lo planes [a_r][a_c] for the Y1 pass
+    float* FL;
 };
 
 // BIG mode (fused Y2+X1): G is never stored as
@@ -68,17 +71,20 @@ __host__ __device__ inline void k1_sizes(int s, int bcap, size_t* sz, bool big =
     sz[9] = 64 * 8;                                     // red
     sz[10] = big ? (size_t)nwarps * kGbufPerWarp * 8 : 0;   // gbuf
     sz[11] = big ? align16((2 * k1_ct_off(s, bcap) + 8) * 8) : 0;   // CP
+    sz[12] = big ? (size_t)nwarps * A * A * 4 : 0;                  // XP
+    sz[13] = big ? (size_t)A * A * 4 : 0;                            // FH
+    sz[14] = big ? (size_t)A * A * 4 : 0;                            // FL
 }
 
 __host__ __device__ inline size_t k1_smem_bytes(int s, int bcap, bool big = false, int nwarps = 0) {
-    size_t sz[12], b = 0;
+    size_t sz[15], b = 0;
     k1_sizes(s, bcap, sz, big, nwarps);
-    for (int k = 0; k < 12; ++k) b += sz[k];
+    for (int k = 0; k < 15; ++k) b += sz[k];
     return b;
 }
 
 __device__ inline K1Lay k1_carve(unsigned char* base, int s, int bcap, bool big = false, int nwarps = 0) {
-    size_t sz[12];
+    size_t sz[15];
     k1_sizes(s, bcap, sz, big, nwarps);
     K1Lay L;
     size_t o = 0;
@@ -93,7 +99,10 @@ __device__ inline K1Lay k1_carve(unsigned char* base, int s, int bcap, bool big 
     L.CT = (float*)(base + o);   o += sz[8];
     L.red = (double*)(base + o); o += sz[9];
     L.gbuf = (float2*)(base + o); o += sz[10];
-    L.CP = (float2*)(base + o);
+    L.CP = (float2*)(base + o); o += sz[11];
+    L.XP = (float*)(base + o); o += sz[12];
+    L.FH = (float*)(base + o); o += sz[13];
+    L.FL = (float*)(base + o);
     return L;
 }
 
@@ -155,6 +164,17 @@ __device__ __forceinline__ void ln_split(float x, const Grid& gq, float& hi, flo
 }
 
 enum { PY1 = 0, PY2 = 1, PX1 = 2, PX2 = 3, PY1S = 4, PY2S = 5 };
+
+// Phase profile (build with -DDD_PHASE_PROF, tools/phase_profile.py): per-warp
+// cycle counters summed over all warps of all cells of a launch, by BIG mode.
+#ifdef DD_PHASE_PROF
+__device__ unsigned long long g_phase[2][16];
+#define PROF_T(v) const long long v = clock64()
+#define PROF_ADD(k, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase[BIG ? 1 : 0][k], (unsigned long long)(v)); } while (0)
+#else
+#define PROF_T(v) do {} while (0)
+#define PROF_ADD(k, v) do {} while (0)
+#endif
 
 __device__ __forceinline__ float grp_sum(float v, unsigned mask, int G) {
     for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
@@ -416,7 +436,7 @@ __device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y
 template <int NT, int AR, int NQ>
 __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all,
                                            const float2* __restrict__ LNUg, float* __restrict__ SLg,
-                                           int& fallbacks, int& nonfinite) {
+                                           const float2* __restrict__ Fcur, int& fallbacks, int& nonfinite) {
     constexpr int RG = kRG;
     constexpr int YS = 32 / (RG * NQ);      // phase-B lanes sharing one output (y2 split)
     constexpr int SUB = 32 / YS;            // y2 per phase-B lane slice of a chunk
@@ -434,6 +454,25 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
     const float2 L2E2 = make_float2(kL2E, kL2E);
     const float2* CP = L.CP;
 
+    // fused X2 partial sums: lane owns outputs (x1a + h, x2q + j), h < 2, j < 4;
+    // stabiliser = the previous X2 LSE, LM - F (speculative, as the PX2 pass)
+    const int npair = d.ar >> 1;
+    const int xi1 = lane % npair, xiq = lane / npair;
+    const int x1a = 2 * xi1, x2q = 4 * xiq;
+    const bool xvalid = x2q < d.ac;
+    float2 nSX[4], XA[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        XA[j] = make_float2(0.f, 0.f);
+        float sx0 = 0.f, sx1 = 0.f;
+        if (xvalid) {
+            const float2 f0 = Fcur[x1a * d.pX + x2q + j], f1 = Fcur[(x1a + 1) * d.pX + x2q + j];
+            const float l0 = L.LM[x1a * d.ac + x2q + j].x, l1 = L.LM[(x1a + 1) * d.ac + x2q + j].x;
+            if (f0.x > -INFINITY && l0 > -INFINITY) sx0 = l0 - f0.x;
+            if (f1.x > -INFINITY && l1 > -INFINITY) sx1 = l1 - f1.x;
+        }
+        nSX[j] = make_float2(-sx0, -sx1);
+    }
     for (int grp = warp; grp < ngroups; grp += NT / 32) {
         const int y1b = grp * RG;
         const int y1B = y1b + rB;
@@ -668,18 +707,198 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
             }
         }
         __syncwarp();
+        // fused X2: partial LSE over this group's rows, F_new(x1, x2) needs
+        // sum_y1 exp(U(y1, x2) - C(y1 - x1) - S(x1, x2))
+        if (xvalid) {
+            for (int r = 0; r < RG && y1b + r < d.br; ++r) {
+                const int y1 = y1b + r;
+                const float2 cpr = CP[d.off + y1 - x1a];     // (C(x1a - y1), C(x1a + 1 - y1))
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float2 u = L.Ut[(x2q + j) * d.pU + y1];
+                    float2 t = __fadd2_rn(make_float2(u.x, u.x), neg2(cpr));
+                    t = __fadd2_rn(t, nSX[j]);
+                    t = __ffma2_rn(t, L2E2, make_float2(u.y, u.y));
+                    XA[j] = __fadd2_rn(XA[j], make_float2(ex2f(t.x), ex2f(t.y)));
+                }
+            }
+        }
+    }
+    // per-warp partials -> SMEM (every warp writes all of its slots)
+    {
+        float* xp = L.XP + warp * (d.ar * d.ac);
+        for (int o = lane; o < d.ar * d.ac; o += 32) xp[o] = 0.f;
+        __syncwarp();
+        if (xvalid) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                xp[x1a * d.ac + x2q + j] = XA[j].x;
+                xp[(x1a + 1) * d.ac + x2q + j] = XA[j].y;
+            }
+        }
+    }
+}
+
+
+// BIG: the first Y half-pass T(x1, y2) = LSE_x2[F(x1, x2) - C(x2 - y2)].
+// Work units (32-column chunk, x1 pair) round-robin over warps (balanced:
+// #units is a multiple of a_r/2); lane <-> y2; the F row pair is read as
+// broadcast 128-bit loads from the hi/lo planes, the per-lane cost pair
+// (C(x2 - y2), C(x2 + 1 - y2)) from CP; speculative stabiliser = previous T
+// (exact two-pass on the first iteration or when the window check fails).
+template <int NT>
+__device__ void y1_big(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all, int& fallbacks,
+                       int& nonfinite) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int npair = d.ar >> 1;
+    const int nchunks = (d.bc + 31) >> 5;
+    const int nunits = nchunks * npair;
+    const float2 L2E2 = make_float2(kL2E, kL2E);
+    for (int u = warp; u < nunits; u += NT / 32) {
+        const int c = u / npair, pr = u % npair;
+        const int y2 = 32 * c + lane;
+        const bool vy = y2 < d.bc;
+        const int y2c = vy ? y2 : d.bc - 1;
+        const int x1 = 2 * pr;
+        float2* Tc = L.Tt + y2c * d.pT;
+        const float2* cpp = L.CP + d.off + y2c;           // cpp[-x2] = (C(x2 - y2), C(x2 + 1 - y2))
+        const float* fh0 = L.FH + x1 * d.ac;
+        const float* fh1 = fh0 + d.ac;
+        const float* fl0 = L.FL + x1 * d.ac;
+        const float* fl1 = fl0 + d.ac;
+        float S0, S1;
+        bool exact = exact_all;
+        if (!exact) {
+            S0 = Tc[x1].x;
+            S1 = Tc[x1 + 1].x;
+            exact = !(fabsf(S0) < 1e30f) || !(fabsf(S1) < 1e30f);
+        }
+        float s0 = 0.f, s1 = 0.f;
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            if (exact) {
+                float M0 = -INFINITY, M1 = -INFINITY;
+                for (int x2 = 0; x2 < d.ac; x2 += 2) {
+                    const float2 cp = cpp[-x2];
+                    const float2 a = __fadd2_rn(*reinterpret_cast<const float2*>(fh0 + x2), neg2(cp));
+                    const float2 b = __fadd2_rn(*reinterpret_cast<const float2*>(fh1 + x2), neg2(cp));
+                    M0 = fmax3f(M0, a.x, a.y);
+                    M1 = fmax3f(M1, b.x, b.y);
+                }
+                S0 = M0 > -INFINITY ? M0 : 0.f;
+                S1 = M1 > -INFINITY ? M1 : 0.f;
+            }
+            float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+            const float2 nS0 = make_float2(-S0, -S0), nS1 = make_float2(-S1, -S1);
+#pragma unroll 2
+            for (int x2 = 0; x2 < d.ac; x2 += 4) {
+                const float4 h0 = *reinterpret_cast<const float4*>(fh0 + x2);
+                const float4 h1 = *reinterpret_cast<const float4*>(fh1 + x2);
+                const float4 l0 = *reinterpret_cast<const float4*>(fl0 + x2);
+                const float4 l1 = *reinterpret_cast<const float4*>(fl1 + x2);
+                const float2 cpa = cpp[-x2], cpb = cpp[-x2 - 2];
+                float2 t;
+                t = __ffma2_rn(__fadd2_rn(__fadd2_rn(make_float2(h0.x, h0.y), neg2(cpa)), nS0), L2E2, make_float2(l0.x, l0.y));
+                a0 = __fadd2_rn(a0, make_float2(ex2f(t.x), ex2f(t.y)));
+                t = __ffma2_rn(__fadd2_rn(__fadd2_rn(make_float2(h0.z, h0.w), neg2(cpb)), nS0), L2E2, make_float2(l0.z, l0.w));
+                a0 = __fadd2_rn(a0, make_float2(ex2f(t.x), ex2f(t.y)));
+                t = __ffma2_rn(__fadd2_rn(__fadd2_rn(make_float2(h1.x, h1.y), neg2(cpa)), nS1), L2E2, make_float2(l1.x, l1.y));
+                a1 = __fadd2_rn(a1, make_float2(ex2f(t.x), ex2f(t.y)));
+                t = __ffma2_rn(__fadd2_rn(__fadd2_rn(make_float2(h1.z, h1.w), neg2(cpb)), nS1), L2E2, make_float2(l1.z, l1.w));
+                a1 = __fadd2_rn(a1, make_float2(ex2f(t.x), ex2f(t.y)));
+            }
+            s0 = a0.x + a0.y;
+            s1 = a1.x + a1.y;
+            if (exact) break;
+            const bool ok = (s0 >= 0.25f && s0 <= 4.0f) && (s1 >= 0.25f && s1 <= 4.0f);
+            if (ok) break;
+            exact = true;
+            ++fallbacks;
+        }
+        if (vy) {
+            float2 t0 = make_float2(-INFINITY, 0.f), t1 = make_float2(-INFINITY, 0.f);
+            if (s0 > 1e-37f) {
+                const float l2 = lg2f(s0);
+                const float lh = gridq(l2 * kLN2, gq);
+                t0 = make_float2(S0 + lh, fmaf(-lh, kL2E, l2));
+                if (!(fabsf(t0.x) < 1e30f)) nonfinite = 1;
+            }
+            if (s1 > 1e-37f) {
+                const float l2 = lg2f(s1);
+                const float lh = gridq(l2 * kLN2, gq);
+                t1 = make_float2(S1 + lh, fmaf(-lh, kL2E, l2));
+                if (!(fabsf(t1.x) < 1e30f)) nonfinite = 1;
+            }
+            Tc[x1] = t0;
+            Tc[x1 + 1] = t1;
+        }
+    }
+}
+
+// BIG: finalise the X-iteration from the fused per-warp partial sums
+// (fixed warp order): F_new = log mu - (S + ln sum) with S = LM - F; an
+// output whose sum leaves [1/4, 4] is recomputed with an exact max over y1.
+// Accumulates the L1 X-error of the plan (F, G) as the PX2 pass.
+template <int NT>
+__device__ void x2_finalize(const K1Lay& L, const Dims& d, const Grid& gq, const float2* Fcur, float2* Fout,
+                            double& err_acc, int& fallbacks, int& nonfinite) {
+    const int nx = d.ar * d.ac;
+    for (int o = threadIdx.x; o < nx; o += NT) {
+        const int x1 = o / d.ac, x2 = o % d.ac;
+        const float2 lm = L.LM[o];
+        const float2 fo = Fcur[x1 * d.pX + x2];
+        if (lm.x == -INFINITY) {
+            Fout[x1 * d.pX + x2] = make_float2(-INFINITY, 0.f);
+            L.FH[o] = -INFINITY;
+            L.FL[o] = 0.f;
+            continue;
+        }
+        float S = (fo.x > -INFINITY) ? lm.x - fo.x : 0.f;
+        float s = 0.f;
+        for (int w = 0; w < NT / 32; ++w) s += L.XP[w * nx + o];
+        if (!(s >= 0.25f && s <= 4.0f)) {
+            // exact recompute over y1 of U(y1, x2) - C(y1 - x1)
+            const float2* Ur = L.Ut + x2 * d.pU;
+            const float* ctp = L.CT + d.off - x1;        // C(y1 - x1) = ctp[y1]
+            float M = -INFINITY;
+            for (int y = 0; y < d.br; ++y) M = fmaxf(M, Ur[y].x - ctp[y]);
+            s = 0.f;
+            if (M > -INFINITY)
+                for (int y = 0; y < d.br; ++y) {
+                    const float2 u = Ur[y];
+                    s += ex2f(((u.x - ctp[y]) - M) * kL2E + u.y);
+                }
+            S = M;
+            ++fallbacks;
+        }
+        if (!(s > 1e-37f) || !(S > -INFINITY)) {
+            nonfinite = 1;
+            Fout[x1 * d.pX + x2] = make_float2(-INFINITY, 0.f);
+            L.FH[o] = -INFINITY;
+            L.FL[o] = 0.f;
+            continue;
+        }
+        float lh, ll;
+        ln_split(s, gq, lh, ll);
+        const float2 fn = make_float2(lm.x - (S + lh), lm.y - ll);
+        Fout[x1 * d.pX + x2] = fn;
+        L.FH[o] = fn.x;
+        L.FL[o] = fn.y;
+        if (!(fabsf(fn.x) < 1e30f)) nonfinite = 1;
+        // P_X pi(x) = mu(x) exp(F - F_new)  (plan (F, G))
+        const float dF = (fo.x - fn.x) + (fo.y - fn.y) * kLN2;
+        err_acc += (double)L.MU[o] * (double)fabsf(expm1f(dF));
     }
 }
 
 template <int NT>
 __device__ void fused_dispatch(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all,
-                               const float2* LNUg, float* SLg, int& fb, int& nf) {
+                               const float2* LNUg, float* SLg, const float2* Fcur, int& fb, int& nf) {
     if (d.ar > 8) {
-        if (d.ac > 8) fused_y2x1<NT, 16, 4>(L, d, gq, exact_all, LNUg, SLg, fb, nf);
-        else fused_y2x1<NT, 16, 2>(L, d, gq, exact_all, LNUg, SLg, fb, nf);
+        if (d.ac > 8) fused_y2x1<NT, 16, 4>(L, d, gq, exact_all, LNUg, SLg, Fcur, fb, nf);
+        else fused_y2x1<NT, 16, 2>(L, d, gq, exact_all, LNUg, SLg, Fcur, fb, nf);
     } else {
-        if (d.ac > 8) fused_y2x1<NT, 8, 4>(L, d, gq, exact_all, LNUg, SLg, fb, nf);
-        else fused_y2x1<NT, 8, 2>(L, d, gq, exact_all, LNUg, SLg, fb, nf);
+        if (d.ac > 8) fused_y2x1<NT, 8, 4>(L, d, gq, exact_all, LNUg, SLg, Fcur, fb, nf);
+        else fused_y2x1<NT, 8, 2>(L, d, gq, exact_all, LNUg, SLg, Fcur, fb, nf);
     }
 }
 
@@ -843,6 +1062,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
             lm = split_hl(p.logmu[g], gq);
         }
         L.FX[(x / d.ac) * d.pX + x % d.ac] = f;
+        if (BIG) { L.FH[x] = f.x; L.FL[x] = f.y; }
         L.LM[x] = lm;
         L.MU[x] = (float)m;
     }
@@ -878,26 +1098,42 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     float2* Fn = L.FXn;
     int it = 0, fallbacks = 0, nonfinite = 0;
     double err = 0.0;
+    PROF_T(t_loop0);
     while (true) {
         const bool exact = (it == 0);
         double e_loc = 0.0;
-        lse_pass<PY1, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
+        PROF_T(ta);
+        if (BIG) y1_big<NT>(L, d, gq, exact, fallbacks, nonfinite);
+        else lse_pass<PY1, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
+        PROF_T(tb);
         __syncthreads();
+        PROF_T(tc);
         if (BIG) {
-            fused_dispatch<NT>(L, d, gq, exact, LNU, SLg, fallbacks, nonfinite);
+            fused_dispatch<NT>(L, d, gq, exact, LNU, SLg, Fc, fallbacks, nonfinite);
         } else {
             lse_pass<PY2, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
             __syncthreads();
             lse_pass<PX1, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
         }
+        PROF_T(td);
         __syncthreads();
-        lse_pass<PX2, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
+        PROF_T(te);
+        if (BIG) x2_finalize<NT>(L, d, gq, Fc, Fn, e_loc, fallbacks, nonfinite);
+        else lse_pass<PX2, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
+        PROF_T(tf);
         err = block_sum(e_loc, L.red);      // includes the barrier
+        PROF_T(tg);
+        // per warp: busy time of the passes and barrier waits (phase profile build only)
+        PROF_ADD(0, tb - ta); PROF_ADD(1, tc - tb); PROF_ADD(2, td - tc); PROF_ADD(3, te - td);
+        PROF_ADD(4, tf - te); PROF_ADD(5, tg - tf);
         ++it;
         if (err <= tol) break;
         if (it >= p.max_iter || !(err == err)) { co.flags |= 1; break; }
         float2* t = Fc; Fc = Fn; Fn = t;
     }
+    PROF_T(t_loop1);
+    PROF_ADD(6, t_loop1 - t_loop0);
+    PROF_ADD(7, t_loop0 - t_start);
     // ---- line 10: extraction from the plan (F, G): exact Y-iteration with
     // the row sums split by basic-cell quadrant (x1 half, x2 half)
     {
@@ -1071,6 +1307,8 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     if (tid == 0) {
         if (s_newoff[0] < 0) co.flags |= 8;
         co.pad = (int)min((clock64() - t_start) >> 10, (long long)0x7fffffff);   // solve time, kcycles
+        PROF_ADD(8, clock64() - t_loop1);
+        PROF_ADD(9, it);
         p.out[cell] = co;
     }
 }
@@ -1145,6 +1383,19 @@ __global__ void k0_sort(const int* lists, const int* counts, int ncap, const int
         const int c = in[k];
         out[atomicAdd(&hist[1023 - min(bside[c], 1023)], 1)] = c;
     }
+}
+
+// Read (and reset) the phase profile counters; zeros unless built with -DDD_PHASE_PROF.
+cudaError_t k1_phase_read(unsigned long long* out32) {
+#ifdef DD_PHASE_PROF
+    cudaError_t e = cudaMemcpyFromSymbol(out32, g_phase, sizeof(g_phase));
+    if (e != cudaSuccess) return e;
+    unsigned long long z[32] = {0};
+    return cudaMemcpyToSymbol(g_phase, z, sizeof(g_phase));
+#else
+    for (int k = 0; k < 32; ++k) out32[k] = 0;
+    return cudaSuccess;
+#endif
 }
 
 size_t k1_smem_bytes_host(int s, int bcap, bool big, int nwarps) { return k1_smem_bytes(s, bcap, big, nwarps); }

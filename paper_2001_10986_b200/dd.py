@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libdd_gpu.so")
+SO_PATH = os.environ.get("DD_LIB", os.path.join(_HERE, "libdd_gpu.so"))   # DD_LIB: diagnostic builds
 
 OK, EINVAL, ENOCONV, ENUMERIC, ECUDA, ENCCL, ENOMEM = 0, 1, 2, 3, 4, 5, 6
 COST_SQEUCLID = 0
@@ -23,7 +23,7 @@ PLAN_BASIC_MARGINALS, PLAN_COO = 0, 1
 # every symbol include/dd.h declares (checked by tests/test_abi.py)
 EXPORTS = ["dd_init", "dd_iterate", "dd_set_eps", "dd_refine", "dd_run_schedule", "dd_reset",
            "dd_primal_cost", "dd_marginal_error", "dd_fetch_plan", "dd_get_stats", "dd_get_totals",
-           "dd_reset_totals", "dd_get_cell_stats", "dd_get_state_info", "dd_get_state", "dd_set_state",
+           "dd_reset_totals", "dd_phase_profile", "dd_get_cell_stats", "dd_get_state_info", "dd_get_state", "dd_set_state",
            "dd_build_schedule", "dd_measure_mufu_peak", "dd_synchronize", "dd_free",
            "dd_last_error", "dd_version"]
 
@@ -75,6 +75,7 @@ def lib():
         L.dd_get_totals.argtypes = [p, C.POINTER(SweepStats)]
         L.dd_reset_totals.argtypes = [p]
         L.dd_get_cell_stats.argtypes = [p, p, p, p, p, i]
+        L.dd_phase_profile.argtypes = [p, p]
         L.dd_get_state_info.argtypes = [p, C.POINTER(StateInfo)]
         L.dd_get_state.argtypes = [p, p, p, p, p, p]
         L.dd_set_state.argtypes = [p, i, ll, i, p, p, p, ll, p, p]
@@ -210,6 +211,12 @@ class DD:
 
     def reset_totals(self):
         return self._check(lib().dd_reset_totals(self._h), "reset_totals")
+
+    def phase_profile(self):
+        """K1 per-phase cycle counters since the last call ([2][16] uint64; see dd.h)."""
+        out = np.zeros(32, np.uint64)
+        self._check(lib().dd_phase_profile(self._h, out.ctypes.data), "phase_profile")
+        return out.reshape(2, 16)
 
     def cell_stats(self):
         """Per composite cell of the last sweep: (iters, box_side, mufu_ops, kcycles) arrays."""

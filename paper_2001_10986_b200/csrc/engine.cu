@@ -191,7 +191,7 @@ int check_overflow(dd_ctx* c) {
 constexpr int kCap1 = 120, kCap2 = 704;   // tier-1 cap 120: measured best split
 constexpr size_t kSmem1 = 110 * 1024, kSmem2 = 220 * 1024;
 void tier_caps(int s, int opt_main, int opt_big, int* b0, int* b1, int* b2) {
-    int want = (s <= 4) ? 32 : 40;
+    int want = (s <= 4) ? 32 : 24;   // measured: the fused path wins above ~24 px (s = 8)
     if (opt_main > 0) want = opt_main;
     if (want < 2 * s + 2) want = 2 * s + 2;
     *b0 = want;

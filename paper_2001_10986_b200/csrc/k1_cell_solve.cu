@@ -429,15 +429,13 @@ __device__ __forceinline__ void lse_pass(const K1Lay& L, const Dims& d, const Gr
 // G lives only in a per-warp buffer of one chunk; U is written to Ut[x2][y1]
 // for the X2 pass.  Algorithmic exps: ar br bc (phase A) + br bc ac (phase B)
 // = the Y2 and X1 passes of the separable scheme.
-constexpr int kRG = 4;
 
 __device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
 
-template <int NT, int AR, int NQ>
+template <int NT, int AR, int NQ, int RG>
 __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all,
                                            const float2* __restrict__ LNUg, float* __restrict__ SLg,
                                            const float2* __restrict__ Fcur, int& fallbacks, int& nonfinite) {
-    constexpr int RG = kRG;
     constexpr int YS = 32 / (RG * NQ);      // phase-B lanes sharing one output (y2 split)
     constexpr int SUB = 32 / YS;            // y2 per phase-B lane slice of a chunk
     constexpr int PR = YS * (SUB + 1);      // gbuf row pitch (float2), conflict-free
@@ -893,12 +891,14 @@ __device__ void x2_finalize(const K1Lay& L, const Dims& d, const Grid& gq, const
 template <int NT>
 __device__ void fused_dispatch(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all,
                                const float2* LNUg, float* SLg, const float2* Fcur, int& fb, int& nf) {
+    // row groups of RG = 4 (measured: RG = 2 loses more to per-group overhead
+    // than it gains in last-round balance; RG = 8 the reverse)
     if (d.ar > 8) {
-        if (d.ac > 8) fused_y2x1<NT, 16, 4>(L, d, gq, exact_all, LNUg, SLg, Fcur, fb, nf);
-        else fused_y2x1<NT, 16, 2>(L, d, gq, exact_all, LNUg, SLg, Fcur, fb, nf);
+        if (d.ac > 8) fused_y2x1<NT, 16, 4, 4>(L, d, gq, exact_all, LNUg, SLg, Fcur, fb, nf);
+        else fused_y2x1<NT, 16, 2, 4>(L, d, gq, exact_all, LNUg, SLg, Fcur, fb, nf);
     } else {
-        if (d.ac > 8) fused_y2x1<NT, 8, 4>(L, d, gq, exact_all, LNUg, SLg, Fcur, fb, nf);
-        else fused_y2x1<NT, 8, 2>(L, d, gq, exact_all, LNUg, SLg, Fcur, fb, nf);
+        if (d.ac > 8) fused_y2x1<NT, 8, 4, 4>(L, d, gq, exact_all, LNUg, SLg, Fcur, fb, nf);
+        else fused_y2x1<NT, 8, 2, 4>(L, d, gq, exact_all, LNUg, SLg, Fcur, fb, nf);
     }
 }
 

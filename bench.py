@@ -8,9 +8,13 @@ refinements, 72 sweeps of K1 -> K2 -> K3) of one image pair resident in HBM.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 5]
 
-N > 1 (torchrun): each rank solves its own image pair (independent problems,
-no data-path collective; "scaling": "weak"); value = all ranks' cell solves /
-max-over-ranks device time.  Rank 0 prints ONE JSON line.
+N > 1 (torchrun): ONE problem striped over the ranks: each
+rank solves the composite cells of its stripe of basic-cell rows; before and
+after every B-sweep one boundary row moves between neighbouring ranks by NCCL
+send/recv (torch.distributed over NVLink), plus all-reduces of the statistics
+(paper_2001_10986_b200/striped.py).  "scaling": "strong" (fixed total work);
+value = whole-problem cell solves / max-over-ranks device time.  Rank 0
+prints ONE JSON line.
 """
 from __future__ import annotations
 
@@ -40,6 +44,8 @@ def _args():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: host-staged transport, lets N ranks share one GPU (protocol test)")
     return ap.parse_args()
 
 
@@ -160,7 +166,7 @@ def run_reference(args):
     cb["value"] = v
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {**{k: w[k] for k in ("workload", "n", "s")},
                                             "note": "oracle timed on a bounded sample of the workload"},
             "cpu_baseline": cb,
@@ -179,18 +185,23 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(1, torch.cuda.device_count())   # gloo protocol test: ranks may share a GPU
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
+    staging = "cpu" if args.dist_backend == "gloo" else None
 
     from ddinputs import config_images
     from paper_2001_10986_b200 import DD, SCHED_LADDER, measure_mufu_peak
     w = _workload(args.config)
     n, s = w["n"], w["s"]
     eps = w["kappa_final"] / n**2
-    mu_h, nu_h = config_images(args.config, pair=rank)
+    mu_h, nu_h = config_images(args.config, pair=0)      # one problem, striped over the ranks
     mu_d = torch.from_numpy(mu_h).to(dev)
     nu_d = torch.from_numpy(nu_h).to(dev)
     stream = torch.cuda.Stream(dev)          # a real stream handle (the default stream is 0)
@@ -198,11 +209,22 @@ def main():
     kw = dict(err_tol=w["err_tol"], trunc_tau=w["trunc_tau"], schedule=SCHED_LADDER,
               eps_start=w["eps_start"], coarsest_side=w["coarsest"], device=local)
     g = DD(mu_d, nu_d, eps, s, device_input=True, stream=stream.cuda_stream, **kw)
+    run = None
+    if world > 1:
+        from paper_2001_10986_b200.striped import StripedRun, TorchTransport
+        run = StripedRun([(rank, g)], world, TorchTransport(dist, rank, world, dev, staging=staging), device=dev)
+
+    def solve(ctx, striped):
+        """One full coarse-to-fine solve (the bench step)."""
+        if striped is None:
+            ctx.run_schedule()
+        else:
+            striped.run_schedule(n, w["coarsest"], w["kappa_final"], w["eps_start"])
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     for _ in range(args.warmup):
         g.reset()
-        g.run_schedule()
+        solve(g, run)
         g.synchronize()
     # ---- timed region: K steps, per-step CUDA events on the library's stream
     g.reset_totals()
@@ -212,34 +234,39 @@ def main():
     clocks = ClockSampler(local)
     clocks.start()
     step_ms = []
+    cells_step = []
     for _ in range(args.steps):
         flush.fill_(1.0)                       # L2 flush between timed steps (256 MB > 126 MB L2)
         g.reset()                              # state back to the product coupling (untimed)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        c0 = run.cells_solved if run else 0
         e0.record(stream)
-        g.run_schedule()
+        solve(g, run)
         e1.record(stream)
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
+        cells_step.append(run.cells_solved - c0 if run else None)
     torch.cuda.synchronize(dev)
     clk = clocks.stop()
     if world > 1:
         dist.barrier()
     tot = g.totals()
     my_ms = float(np.sum(step_ms))
-    cells_per_step = tot["cells"] / args.steps
-    t = torch.tensor([my_ms, tot["cells"]], dtype=torch.float64, device=dev)
-    if world > 1:
-        tmax = t.clone(); dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        tsum = t.clone(); dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
-        wall_ms, all_cells = float(tmax[0]), float(tsum[1])
+    if run is not None:
+        all_cells = float(np.sum(cells_step))          # whole-problem solves (replicated layers once)
+        wall_ms = float(run.tr.allreduce_max(torch.tensor([my_ms], dtype=torch.float64, device=dev))[0])
     else:
         wall_ms, all_cells = my_ms, float(tot["cells"])
+    cells_per_step = all_cells / args.steps
     value = all_cells / (wall_ms * 1e-3)
     # ---- quality of the final state (outside the timed region)
-    cost, ent = g.primal_cost()
-    l1x, l1y = g.marginal_error()
+    if run is not None:
+        cost, ent = run.primal_cost()
+        l1x, l1y = run.marginal_error()
+    else:
+        cost, ent = g.primal_cost()
+        l1x, l1y = g.marginal_error()
     last = g.stats()
 
     # ---- roofline of the dominant kernel (K1): algorithmic MUFU ops / K1 time
@@ -268,17 +295,27 @@ def main():
         e2e_ms = []
         for k in range(2):
             torch.cuda.synchronize(dev)
+            if world > 1:
+                dist.barrier()
             t0 = time.perf_counter()
             ge = DD(mu_p.numpy(), nu_p.numpy(), eps, s, **kw)
-            ge.run_schedule()
-            c_e, _ = ge.primal_cost()
-            lx_e, ly_e = ge.marginal_error()
+            if run is not None:
+                re = StripedRun([(rank, ge)], world, TorchTransport(dist, rank, world, dev, staging=staging), device=dev)
+                solve(ge, re)
+                c_e, _ = re.primal_cost()
+                lx_e, ly_e = re.marginal_error()
+            else:
+                solve(ge, None)
+                c_e, _ = ge.primal_cost()
+                lx_e, ly_e = ge.marginal_error()
             dt = time.perf_counter() - t0
+            if world > 1:
+                dt = float(run.tr.allreduce_max(torch.tensor([dt], dtype=torch.float64, device=dev))[0])
             ge.close()
             if k > 0:
                 e2e_ms.append(dt * 1e3)
         e2e_ms_med = float(np.median(e2e_ms))
-        e2e = {"value": cells_per_step / (e2e_ms_med * 1e-3) * (world if world > 1 else 1),
+        e2e = {"value": cells_per_step / (e2e_ms_med * 1e-3),
                "unit": UNIT, "h2d_bytes_per_step": int(mu_h.nbytes + nu_h.nbytes),
                "d2h_bytes_per_step": 4 * 8, "ms_per_step": e2e_ms_med,
                "path": "dd_init(host) + dd_run_schedule + dd_primal_cost + dd_marginal_error + dd_free"}
@@ -289,12 +326,13 @@ def main():
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": wall_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "dtype_detail": "f32 ex2/log arithmetic with exact hi/lo argument assembly; f64 staging, "
                             "balance and marginal sums",
             "data": "synthetic",
             "config": {**{k: w[k] for k in ("workload", "n", "s", "kappa_final", "err_tol", "trunc_tau")},
-                       "global_batch": world, "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "global_batch": 1,
+                       "parallelism": f"stripes{world} (NCCL send/recv of boundary rows)" if world > 1 else "single",
                        "l2": "flushed between steps (256 MB write); nu_i pool > L2"},
             "time_to_solution_ms": wall_ms / args.steps,
             "cells_per_step": cells_per_step,

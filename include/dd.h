@@ -165,6 +165,45 @@ int dd_reset_totals(dd_ctx* ctx);
  * cells (<= max_cells are written), or < 0 on error (-DD_E*). */
 int dd_get_cell_stats(dd_ctx* ctx, int* iters, int* box_side, double* mufu_ops, int* kcycles, int max_cells);
 
+/* ---- multi-GPU stripes ----
+ * One context per rank holds the whole layer but solves only the composite
+ * cells of its stripe of basic-cell rows [row_lo, row_hi) (even bounds):
+ * A-cell rows q with 2q in the stripe, B-cell rows q with 2q in the stripe
+ * plus the last B row for the bottom stripe.  Before a B-sweep the row above
+ * the stripe (row_lo - 1) must be imported from the rank above and the
+ * stripe's last row (row_hi - 1) exported to the rank below and cleared;
+ * after it row_lo - 1 goes back (export + clear here, import above).  The
+ * caller moves the byte buffers (NCCL send/recv over NVLink via
+ * torch.distributed in paper_2001_10986_b200/striped.py).  Per-cell
+ * arithmetic does not depend on the stripe: results are bit-identical to
+ * one context for every rank count. */
+
+/* dd_set_stripe -- restrict sweeps and queries of the CURRENT layer to the
+ * stripe; rows outside become empty.  (0, 0) = the whole layer (replicated).
+ * dd_refine and dd_reset return to (0, 0). */
+int dd_set_stripe(dd_ctx* ctx, int row_lo, int row_hi);
+
+/* dd_clear_rows -- mark basic rows [row, row+nrows) empty (owned elsewhere). */
+int dd_clear_rows(dd_ctx* ctx, int row, int nrows);
+
+/* dd_export_rows -- pack basic rows [row, row+nrows) into a DEVICE buffer:
+ * int4 boxes[nrows*nb] | int64 total, int64 count | fp64 values (each box
+ * row-major, padded to an even length).  buf == NULL: *bytes = size needed
+ * (synchronises).  The caller owns buf. */
+int dd_export_rows(dd_ctx* ctx, int row, int nrows, void* buf, size_t* bytes);
+
+/* dd_import_rows -- install rows exported by another context of the same
+ * problem (same layer) from a DEVICE buffer; the values go to the pool's
+ * halo region (one boundary row at a time; DD_ENOMEM if it does not fit). */
+int dd_import_rows(dd_ctx* ctx, int row, int nrows, const void* buf, size_t bytes);
+
+/* dd_y_accumulate -- add this context's sum_i nu_i(y) (2^60 fixed point,
+ * deterministic) into a caller-zeroed DEVICE array acc[side*side] of uint64;
+ * sum the arrays of all ranks (allreduce), then dd_y_l1 gives
+ * l1_y = sum_y |sum_i nu_i(y) - nu(y)| of the whole problem (A18). */
+int dd_y_accumulate(dd_ctx* ctx, unsigned long long* acc);
+int dd_y_l1(dd_ctx* ctx, const unsigned long long* acc, double* l1_y);
+
 /* dd_phase_profile -- diagnostic: per-phase cycle counters of K1 summed over
  * warps since the last call (32 uint64: [mode][16], mode 0 = SMEM tier,
  * 1 = fused big-cell tiers; slots 0..5 = Y1 pass, barrier, Y2+X1, barrier,

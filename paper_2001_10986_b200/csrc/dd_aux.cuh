@@ -15,6 +15,7 @@ struct DevStats {
 
 struct EvalParams {
     int part, side, s, nb, nca;
+    int cr0, cr1;               // cell rows evaluated (multi-GPU stripe)
     double eps;
     const int4* box;
     const long long* off;
@@ -59,6 +60,10 @@ cudaError_t launch_scatter_l1y(const int4* box, const long long* off, const doub
                                unsigned long long* acc, const double* nu, int side, double* partial,
                                double* out, cudaStream_t st);
 cudaError_t launch_eval(const EvalParams& p, int ncells, double* sums, cudaStream_t st);
+cudaError_t launch_scatter_y(const int4* box, const long long* off, const double* pool, int nb,
+                             unsigned long long* acc, int side, cudaStream_t st);
+cudaError_t launch_l1y(const unsigned long long* acc, const double* nu, int side, double* partial, double* out,
+                       cudaStream_t st);
 cudaError_t launch_mufu_bench(float* out, int blocks, int threads, int iters, cudaStream_t st);
 
 }  // namespace dd

@@ -32,6 +32,7 @@ struct SweepParams {
     int part;             // 1 = A, 2 = B
     int side, s, nb, nca; // layer side, basic cell side, basic cells/axis, cells/axis of part
     int ncells;
+    int cr0, cr1;         // cell rows of the partition this context solves (multi-GPU stripe)
     double eps;           // [0,1]^2 units
     double kappa;         // eps / h^2 (squared pixels)
     double tau;           // truncation threshold

@@ -80,6 +80,13 @@ struct dd_ctx {
     double* d_sums = nullptr;       // 4 doubles
     unsigned long long* yacc = nullptr;
     double* partial = nullptr;
+    // multi-GPU stripe of the current layer: basic rows [stripe_lo, stripe_hi)
+    // (0, 0 = the whole layer); imported boundary rows live in the last
+    // halo_cap entries of the pool
+    int stripe_lo = 0, stripe_hi = 0;
+    long long halo_cap = 0;
+    long long* d_xoff = nullptr;    // row export/import offsets scratch
+    long long xoff_n = 0;
     // host bookkeeping
     long long half_index = 0;
     int last_part = 0;
@@ -114,6 +121,15 @@ void set_err(dd_ctx* c, const char* fmt, ...) {
 bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 
 int cells_axis(int nb, int part) { return part == 1 ? nb / 2 : nb / 2 + 1; }
+
+// Partition cell rows [cr0, cr1) a context solves: A-cell row q covers basic
+// rows 2q, 2q+1; B-cell row q covers 2q-1, 2q.  A stripe owns
+// the cells whose LOWER basic row lies in it, plus the last B row at the end.
+void cell_rows(const dd_ctx* c, int part, int nb, int* cr0, int* cr1) {
+    if (c->stripe_hi <= c->stripe_lo) { *cr0 = 0; *cr1 = cells_axis(nb, part); return; }
+    *cr0 = c->stripe_lo / 2;
+    *cr1 = c->stripe_hi / 2 + ((part == 2 && c->stripe_hi == nb) ? 1 : 0);
+}
 
 // Schedule of P:1553-1561 (A12).  Independent of the oracle's copy.
 int build_schedule(int n_final, int coarsest, double kappa_final, double eps_start, int* side, double* kappa,
@@ -231,13 +247,14 @@ int sweep(dd_ctx* c) {
     SweepParams p{};
     p.part = part;
     p.side = Lr.side; p.s = Lr.s; p.nb = Lr.nb; p.nca = nca; p.ncells = ncells;
+    cell_rows(c, part, Lr.nb, &p.cr0, &p.cr1);
     p.eps = c->eps;
     p.kappa = c->eps * (double)Lr.side * (double)Lr.side;
     p.tau = c->tau;
     p.err_tol = c->opt.err_tol;
     p.max_iter = c->opt.max_inner_iter;
     p.box = c->box; p.off = c->off;
-    p.pool_in = c->pool; p.scratch = c->scratch; p.bump = c->bump; p.cap = c->cap;
+    p.pool_in = c->pool; p.scratch = c->scratch; p.bump = c->bump; p.cap = c->cap - c->halo_cap;
     p.alpha = part == 1 ? c->alphaA : c->alphaB;
     p.mu = Lr.mu; p.logmu = Lr.logmu; p.mass_i = Lr.mass;
     p.out = c->cellout;
@@ -279,7 +296,7 @@ int sweep(dd_ctx* c) {
     // K2: deterministic compaction of the new boxes into the pool
     const int nb2 = Lr.nb * Lr.nb;
     CK(launch_scan_areas(c->box, c->off2, c->d_total, nb2, c->d_total + 1, c->st));
-    CK(launch_copy_boxes(c->box, c->off, c->off2, c->scratch, c->pool, nb2, c->cap, c->st));
+    CK(launch_copy_boxes(c->box, c->off, c->off2, c->scratch, c->pool, nb2, c->cap - c->halo_cap, c->st));
     std::swap(c->off, c->off2);
     // K3: fixed-order sweep statistics
     CK(launch_reduce_stats(c->cellout, ncells, c->d_last, c->d_tot, c->d_total + 1, c->counters + 1,
@@ -313,7 +330,7 @@ void free_all(dd_ctx* c) {
     }
     void* ptrs[] = {c->alphaA, c->alphaB, c->box, c->box2, c->off, c->off2, c->pool, c->scratch,
                     c->bump, c->lists, c->bside, c->slices[0], c->slices[1], c->counters, c->cellout, c->d_total, c->d_last, c->d_tot,
-                    c->eval_scratch, c->eval_res, c->d_sums, c->yacc, c->partial};
+                    c->eval_scratch, c->eval_res, c->d_sums, c->yacc, c->partial, c->d_xoff};
     for (void* q : ptrs) if (q) cudaFree(q);
     for (auto& ev : c->pending) for (int k = 0; k < 3; ++k) cudaEventDestroy(ev.e[k]);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -338,6 +355,8 @@ int evaluate(dd_ctx* c, double* out3, bool coo, long long* coo_count, int* cx, i
     // per-cell union boxes on the host (sizes only) for scratch / COO layout
     std::vector<long long> coo_off(ncells + 1, 0);
     int max_ny = 1;
+    int cr0, cr1;
+    cell_rows(c, part, Lr.nb, &cr0, &cr1);
     const int nx_max = 4 * Lr.s * Lr.s;
     for (int cell = 0; cell < ncells; ++cell) {
         const int cp = cell / nca, cq = cell % nca;
@@ -359,7 +378,8 @@ int evaluate(dd_ctx* c, double* out3, bool coo, long long* coo_count, int* cx, i
         const int ny = y1 >= 0 ? (y1 - y0 + 1) * (x1 - x0 + 1) : 0;
         max_ny = std::max(max_ny, ny);
         const int nx = (rhi - rlo + 1) * (chi - clo + 1) * Lr.s * Lr.s;
-        coo_off[cell + 1] = coo_off[cell] + (long long)nx * ny;
+        const bool own = cp >= cr0 && cp < cr1;
+        coo_off[cell + 1] = coo_off[cell] + (own ? (long long)nx * ny : 0LL);
     }
     const long long per_cell = 2LL * max_ny + nx_max;
     const size_t need = (size_t)per_cell * ncells * sizeof(double);
@@ -383,6 +403,7 @@ int evaluate(dd_ctx* c, double* out3, bool coo, long long* coo_count, int* cx, i
     p.mu = Lr.mu; p.logmu = Lr.logmu; p.nu = Lr.nu;
     p.scratch = c->eval_scratch; p.scratch_per_cell = per_cell; p.max_ny = max_ny;
     p.cell_res = c->eval_res;
+    p.cr0 = cr0; p.cr1 = cr1;
     long long* d_coo_off = nullptr;
     int* dx = nullptr;
     int* dy = nullptr;
@@ -565,6 +586,10 @@ int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, d
     const int nbmax = F.nb;
     c->cap = c->opt.pool_capacity > 0 ? c->opt.pool_capacity : 64LL * (long long)n2 + (1LL << 22);
     c->cap = std::max(c->cap, (long long)C0.nb * C0.nb * C0.side * C0.side + 16);
+    // multi-GPU: the last quarter of the pool holds two imported boundary
+    // rows (a row of boxes is <= side^3 / s entries in the product state)
+    c->halo_cap = (c->cap / 3) & ~7LL;   // 16-byte aligned slots
+    c->cap += c->halo_cap;
     CK(cudaMalloc(&c->alphaA, n2 * sizeof(double)));
     CK(cudaMalloc(&c->alphaB, n2 * sizeof(double)));
     CK(cudaMalloc(&c->box, (size_t)nbmax * nbmax * sizeof(int4)));
@@ -626,6 +651,7 @@ int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, d
 int dd_reset(dd_ctx* c) {
     if (!c) return DD_EINVAL;
     c->cur = 0;
+    c->stripe_lo = c->stripe_hi = 0;
     c->eps = (c->opt.schedule == DD_SCHED_LADDER) ? 2.0 / ((double)c->L[0].side * c->L[0].side) : c->eps_final;
     return product_init(c);
 }
@@ -660,6 +686,7 @@ int dd_refine(dd_ctx* c) {
     CK(cudaMemsetAsync(c->alphaB, 0, n2 * sizeof(double), c->st));
     c->launches_pending += 3;
     c->cur += 1;
+    c->stripe_lo = c->stripe_hi = 0;     // the driver sets the fine layer's stripe
     c->last_part = 0;
     return DD_OK;
 }
@@ -721,6 +748,132 @@ int dd_get_totals(dd_ctx* c, dd_sweep_stats* s) {
     s->ms = c->ms_tot;
     s->solve_ms = c->solve_ms_tot;
     s->launches = c->launches_tot;
+    return DD_OK;
+}
+
+int dd_set_stripe(dd_ctx* c, int row_lo, int row_hi) {
+    if (!c) return DD_EINVAL;
+    const Layer& Lr = c->L[c->cur];
+    if (row_lo == 0 && row_hi == 0) { c->stripe_lo = c->stripe_hi = 0; return DD_OK; }
+    if (row_lo < 0 || row_hi > Lr.nb || row_lo >= row_hi || (row_lo & 1) || (row_hi & 1)) {
+        set_err(c, "stripe [%d, %d) must be even basic-row bounds inside [0, %d)", row_lo, row_hi, Lr.nb);
+        return DD_EINVAL;
+    }
+    c->stripe_lo = row_lo;
+    c->stripe_hi = row_hi;
+    // rows outside the stripe become empty (another rank owns them)
+    if (row_lo > 0) CK(cudaMemsetAsync(c->box, 0, (size_t)row_lo * Lr.nb * sizeof(int4), c->st));
+    if (row_hi < Lr.nb)
+        CK(cudaMemsetAsync(c->box + (size_t)row_hi * Lr.nb, 0, (size_t)(Lr.nb - row_hi) * Lr.nb * sizeof(int4), c->st));
+    return DD_OK;
+}
+
+int dd_clear_rows(dd_ctx* c, int row, int nrows) {
+    if (!c) return DD_EINVAL;
+    const Layer& Lr = c->L[c->cur];
+    if (row < 0 || nrows < 0 || row + nrows > Lr.nb) { set_err(c, "rows out of range"); return DD_EINVAL; }
+    if (nrows) CK(cudaMemsetAsync(c->box + (size_t)row * Lr.nb, 0, (size_t)nrows * Lr.nb * sizeof(int4), c->st));
+    return DD_OK;
+}
+
+namespace {
+int ensure_xoff(dd_ctx* c, long long n) {
+    if (n <= c->xoff_n) return DD_OK;
+    if (c->d_xoff) cudaFree(c->d_xoff);
+    c->d_xoff = nullptr;
+    CK(cudaMalloc(&c->d_xoff, (size_t)n * sizeof(long long)));
+    c->xoff_n = n;
+    return DD_OK;
+}
+long long pad2(long long a) { return (a + 1) & ~1LL; }
+}  // namespace
+
+int dd_export_rows(dd_ctx* c, int row, int nrows, void* buf, size_t* bytes) {
+    if (!c || !bytes) return DD_EINVAL;
+    const Layer& Lr = c->L[c->cur];
+    if (row < 0 || nrows <= 0 || row + nrows > Lr.nb) { set_err(c, "rows out of range"); return DD_EINVAL; }
+    int rc = dd_synchronize(c);
+    if (rc) return rc;
+    const int n = nrows * Lr.nb;
+    std::vector<int4> hb(n);
+    CK(cudaMemcpy(hb.data(), c->box + (size_t)row * Lr.nb, n * sizeof(int4), cudaMemcpyDeviceToHost));
+    std::vector<long long> pre(n);
+    long long tot = 0;
+    for (int i = 0; i < n; ++i) { pre[i] = tot; tot += pad2((long long)hb[i].z * hb[i].w); }
+    const size_t need = (size_t)n * sizeof(int4) + 16 + (size_t)tot * sizeof(double);
+    if (!buf) { *bytes = need; return DD_OK; }
+    if (*bytes < need) { set_err(c, "export buffer too small (%zu < %zu)", *bytes, need); return DD_EINVAL; }
+    char* b = (char*)buf;
+    const long long hdr[2] = {tot, n};
+    rc = ensure_xoff(c, n);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(b, c->box + (size_t)row * Lr.nb, n * sizeof(int4), cudaMemcpyDeviceToDevice, c->st));
+    CK(cudaMemcpyAsync(b + (size_t)n * sizeof(int4), hdr, sizeof(hdr), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->d_xoff, pre.data(), n * sizeof(long long), cudaMemcpyHostToDevice, c->st));
+    CK(launch_copy_boxes(c->box + (size_t)row * Lr.nb, c->off + (size_t)row * Lr.nb, c->d_xoff, c->pool,
+                         (double*)(b + (size_t)n * sizeof(int4) + 16), n, tot, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    *bytes = need;
+    return DD_OK;
+}
+
+int dd_import_rows(dd_ctx* c, int row, int nrows, const void* buf, size_t bytes) {
+    if (!c || !buf) return DD_EINVAL;
+    const Layer& Lr = c->L[c->cur];
+    if (row < 0 || nrows <= 0 || row + nrows > Lr.nb) { set_err(c, "rows out of range"); return DD_EINVAL; }
+    int rc = dd_synchronize(c);
+    if (rc) return rc;
+    const int n = nrows * Lr.nb;
+    const char* b = (const char*)buf;
+    if (bytes < (size_t)n * sizeof(int4) + 16) { set_err(c, "import buffer too small"); return DD_EINVAL; }
+    std::vector<int4> hb(n);
+    long long hdr[2];
+    CK(cudaMemcpy(hb.data(), b, n * sizeof(int4), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hdr, b + (size_t)n * sizeof(int4), sizeof(hdr), cudaMemcpyDeviceToHost));
+    std::vector<long long> pre(2 * (size_t)n);
+    long long tot = 0;
+    for (int i = 0; i < n; ++i) {
+        if (hb[i].z < 0 || hb[i].w < 0 || hb[i].x < 0 || hb[i].y < 0 || hb[i].x + hb[i].z > Lr.side ||
+            hb[i].y + hb[i].w > Lr.side) { set_err(c, "imported box %d out of range", i); return DD_EINVAL; }
+        pre[i] = tot;
+        tot += pad2((long long)hb[i].z * hb[i].w);
+    }
+    if (hdr[0] != tot || hdr[1] != n || bytes < (size_t)n * sizeof(int4) + 16 + (size_t)tot * sizeof(double)) {
+        set_err(c, "import header mismatch");
+        return DD_EINVAL;
+    }
+    // two halo slots: rows above the stripe (the B-cells' upper row) and the
+    // stripe's own rows returned by the rank below (both may be live at once)
+    const long long slot = c->halo_cap / 2;
+    if (tot > slot) { set_err(c, "imported rows (%lld entries) exceed the halo slot %lld", tot, slot); return DD_ENOMEM; }
+    const long long hbase = c->cap - c->halo_cap + ((row < c->stripe_lo) ? 0 : slot);
+    for (int i = 0; i < n; ++i) pre[n + i] = hbase + pre[i];
+    rc = ensure_xoff(c, 2LL * n);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(c->box + (size_t)row * Lr.nb, b, n * sizeof(int4), cudaMemcpyDeviceToDevice, c->st));
+    CK(cudaMemcpyAsync(c->d_xoff, pre.data(), 2 * (size_t)n * sizeof(long long), cudaMemcpyHostToDevice, c->st));
+    CK(launch_copy_boxes(c->box + (size_t)row * Lr.nb, c->d_xoff, c->d_xoff + n,
+                         (const double*)(b + (size_t)n * sizeof(int4) + 16), c->pool, n, c->cap, c->st));
+    CK(cudaMemcpyAsync(c->off + (size_t)row * Lr.nb, c->d_xoff + n, n * sizeof(long long), cudaMemcpyDeviceToDevice,
+                       c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return DD_OK;
+}
+
+int dd_y_accumulate(dd_ctx* c, unsigned long long* acc) {
+    if (!c || !acc) return DD_EINVAL;
+    const Layer& Lr = c->L[c->cur];
+    CK(launch_scatter_y(c->box, c->off, c->pool, Lr.nb, acc, Lr.side, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return DD_OK;
+}
+
+int dd_y_l1(dd_ctx* c, const unsigned long long* acc, double* l1_y) {
+    if (!c || !acc || !l1_y) return DD_EINVAL;
+    const Layer& Lr = c->L[c->cur];
+    CK(launch_l1y(acc, Lr.nu, Lr.side, c->partial, c->d_sums + 3, c->st));
+    CK(cudaMemcpyAsync(l1_y, c->d_sums + 3, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
     return DD_OK;
 }
 

@@ -1343,6 +1343,13 @@ __global__ void k0_classify(SweepParams p, int b0, int b1, int* lists, int* coun
     const int cell = blockIdx.x * blockDim.x + threadIdx.x;
     if (cell >= p.ncells) return;
     const int cp = cell / p.nca, cq = cell % p.nca;
+    if (cp < p.cr0 || cp >= p.cr1) {      // another rank's stripe: no solve, zero statistics
+        CellOut z;
+        z.iters = 0; z.flags = 0; z.err = 0.f; z.box = 0; z.mufu = 0.0; z.fallbacks = 0; z.pad = 0;
+        p.out[cell] = z;
+        bside[cell] = 0;
+        return;
+    }
     int rlo, rhi, clo, chi;
     cell_span(p.nb, p.part, cp, rlo, rhi);
     cell_span(p.nb, p.part, cq, clo, chi);

@@ -114,6 +114,7 @@ __global__ void k_copy_boxes(const int4* __restrict__ box, const long long* __re
 __global__ void k_reduce_stats(const CellOut* __restrict__ out, int ncells, DevStats* last, DevStats* tot,
                                const long long* __restrict__ entries, const int* __restrict__ n_deferred,
                                const int* __restrict__ overflow, const int* __restrict__ n_huge) {
+    // cells solved = the three tier counts (n_deferred - 1 .. n_huge); others are zero rows
     __shared__ double s_err[1024], s_mufu[1024];
     __shared__ long long s_it[1024], s_fb[1024];
     __shared__ int s_max[1024], s_fail[1024], s_box[1024];
@@ -147,7 +148,7 @@ __global__ void k_reduce_stats(const CellOut* __restrict__ out, int ncells, DevS
     }
     if (t == 0) {
         DevStats L;
-        L.cells = ncells;
+        L.cells = (long long)n_deferred[-1] + n_deferred[0] + n_huge[0];
         L.iters_sum = s_it[0];
         L.iters_max = s_max[0];
         L.failed = s_fail[0];
@@ -268,6 +269,10 @@ __global__ void k_eval_cells(EvalParams p) {
     const int cell = blockIdx.x;
     const int tid = threadIdx.x;
     const int cp = cell / p.nca, cq = cell % p.nca;
+    if (cp < p.cr0 || cp >= p.cr1) {          // another rank's stripe
+        if (tid < 3) p.cell_res[3 * cell + tid] = 0.0;
+        return;
+    }
     int rlo, rhi, clo, chi;
     cell_span(p.nb, p.part, cp, rlo, rhi);
     cell_span(p.nb, p.part, cq, clo, chi);
@@ -450,6 +455,19 @@ cudaError_t launch_scatter_l1y(const int4* box, const long long* off, const doub
     LAUNCH_CHECK();
     const int nblk = 256;
     k_l1_y<<<nblk, 256, 0, st>>>(acc, nu, n2, partial);
+    LAUNCH_CHECK();
+    k_sum<<<1, 256, 0, st>>>(partial, nblk, 1, out);
+    LAUNCH_CHECK(); return cudaSuccess;
+}
+cudaError_t launch_scatter_y(const int4* box, const long long* off, const double* pool, int nb,
+                             unsigned long long* acc, int side, cudaStream_t st) {
+    k_scatter_y<<<nb * nb, 256, 0, st>>>(box, off, pool, acc, side);
+    LAUNCH_CHECK(); return cudaSuccess;
+}
+cudaError_t launch_l1y(const unsigned long long* acc, const double* nu, int side, double* partial, double* out,
+                       cudaStream_t st) {
+    const int nblk = 256;
+    k_l1_y<<<nblk, 256, 0, st>>>(acc, nu, (long long)side * side, partial);
     LAUNCH_CHECK();
     k_sum<<<1, 256, 0, st>>>(partial, nblk, 1, out);
     LAUNCH_CHECK(); return cudaSuccess;

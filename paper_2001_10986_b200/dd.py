@@ -23,7 +23,8 @@ PLAN_BASIC_MARGINALS, PLAN_COO = 0, 1
 # every symbol include/dd.h declares (checked by tests/test_abi.py)
 EXPORTS = ["dd_init", "dd_iterate", "dd_set_eps", "dd_refine", "dd_run_schedule", "dd_reset",
            "dd_primal_cost", "dd_marginal_error", "dd_fetch_plan", "dd_get_stats", "dd_get_totals",
-           "dd_reset_totals", "dd_phase_profile", "dd_get_cell_stats", "dd_get_state_info", "dd_get_state", "dd_set_state",
+           "dd_reset_totals", "dd_set_stripe", "dd_clear_rows", "dd_export_rows",
+           "dd_import_rows", "dd_y_accumulate", "dd_y_l1", "dd_phase_profile", "dd_get_cell_stats", "dd_get_state_info", "dd_get_state", "dd_set_state",
            "dd_build_schedule", "dd_measure_mufu_peak", "dd_synchronize", "dd_free",
            "dd_last_error", "dd_version"]
 
@@ -76,6 +77,12 @@ def lib():
         L.dd_reset_totals.argtypes = [p]
         L.dd_get_cell_stats.argtypes = [p, p, p, p, p, i]
         L.dd_phase_profile.argtypes = [p, p]
+        L.dd_set_stripe.argtypes = [p, i, i]
+        L.dd_clear_rows.argtypes = [p, i, i]
+        L.dd_export_rows.argtypes = [p, i, i, p, C.POINTER(C.c_size_t)]
+        L.dd_import_rows.argtypes = [p, i, i, p, C.c_size_t]
+        L.dd_y_accumulate.argtypes = [p, p]
+        L.dd_y_l1.argtypes = [p, p, C.POINTER(d)]
         L.dd_get_state_info.argtypes = [p, C.POINTER(StateInfo)]
         L.dd_get_state.argtypes = [p, p, p, p, p, p]
         L.dd_set_state.argtypes = [p, i, ll, i, p, p, p, ll, p, p]
@@ -211,6 +218,36 @@ class DD:
 
     def reset_totals(self):
         return self._check(lib().dd_reset_totals(self._h), "reset_totals")
+
+    # ---- multi-GPU stripe primitives (device buffers: objects with data_ptr())
+    def set_stripe(self, row_lo, row_hi):
+        return self._check(lib().dd_set_stripe(self._h, row_lo, row_hi), "set_stripe")
+
+    def clear_rows(self, row, nrows):
+        return self._check(lib().dd_clear_rows(self._h, row, nrows), "clear_rows")
+
+    def export_rows_size(self, row, nrows):
+        nbytes = C.c_size_t(0)
+        self._check(lib().dd_export_rows(self._h, row, nrows, None, C.byref(nbytes)), "export_rows")
+        return nbytes.value
+
+    def export_rows(self, row, nrows, dev_buf):
+        nbytes = C.c_size_t(int(dev_buf.numel() * dev_buf.element_size()))
+        self._check(lib().dd_export_rows(self._h, row, nrows, C.c_void_p(dev_buf.data_ptr()),
+                                         C.byref(nbytes)), "export_rows")
+        return nbytes.value
+
+    def import_rows(self, row, nrows, dev_buf, nbytes):
+        return self._check(lib().dd_import_rows(self._h, row, nrows, C.c_void_p(dev_buf.data_ptr()), nbytes),
+                           "import_rows")
+
+    def y_accumulate(self, dev_acc):
+        return self._check(lib().dd_y_accumulate(self._h, C.c_void_p(dev_acc.data_ptr())), "y_accumulate")
+
+    def y_l1(self, dev_acc):
+        v = C.c_double(0)
+        self._check(lib().dd_y_l1(self._h, C.c_void_p(dev_acc.data_ptr()), C.byref(v)), "y_l1")
+        return v.value
 
     def phase_profile(self):
         """K1 per-phase cycle counters since the last call ([2][16] uint64; see dd.h)."""

@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_striped_gpu.py -x -q > gpurun_out/pytest_striped.log 2>&1; echo striped rc=$?
+tail -30 gpurun_out/pytest_striped.log

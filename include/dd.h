@@ -77,7 +77,9 @@ typedef struct {                /* zero-initialised fields take the defaults */
     void* stream;               /* cudaStream_t to use, or NULL */
     int reserved[8];            /* [0] > 0: box-side cap of the SMEM tier (tier 0);
                                    [1] > 0: box-side cap of the 2-CTA/SM fused tier (tier 1);
-                                   testing knobs that route cells to the other K1 tiers */
+                                   testing knobs that route cells to the other K1 tiers;
+                                   [2] = 1: cold-start potentials at dd_refine (reading A14)
+                                   instead of the glued + interpolated warm start */
 } dd_options;
 
 typedef struct {                /* one sweep (or accumulated totals) */
@@ -124,7 +126,10 @@ int dd_iterate(dd_ctx* ctx, int n_half_iters);
 int dd_set_eps(dd_ctx* ctx, double eps);
 
 /* dd_refine -- move to the next finer layer: nu_i^0 by eq. FineBasicMarginals
- * (P:1471-1474); alpha cold start (reading A14). */
+ * (P:1471-1474); alpha warm start = the coarse potentials glued by the
+ * discrete Helmholtz least squares and interpolated linearly in
+ * log space, or a cold start (alpha = 0, reading A14) when
+ * dd_options.reserved[2] = 1 or a multi-GPU stripe is set. */
 int dd_refine(dd_ctx* ctx);
 
 /* dd_run_schedule -- LADDER mode: run the whole schedule (refinements, eps

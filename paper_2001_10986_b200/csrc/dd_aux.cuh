@@ -64,6 +64,9 @@ cudaError_t launch_scatter_y(const int4* box, const long long* off, const double
                              unsigned long long* acc, int side, cudaStream_t st);
 cudaError_t launch_l1y(const unsigned long long* acc, const double* nu, int side, double* partial, double* out,
                        cudaStream_t st);
+cudaError_t launch_glue_refine(const double* aA_c, const double* aB_c, const double* mu_c, int side_c, int s_c,
+                               double eps, double* scratch, double* aA_f, double* aB_f, cudaStream_t st);
+size_t glue_scratch_doubles(int side_c, int s_c);
 cudaError_t launch_mufu_bench(float* out, int blocks, int threads, int iters, cudaStream_t st);
 
 }  // namespace dd

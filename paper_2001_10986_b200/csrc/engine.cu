@@ -86,6 +86,7 @@ struct dd_ctx {
     int stripe_lo = 0, stripe_hi = 0;
     long long halo_cap = 0;
     long long* d_xoff = nullptr;    // row export/import offsets scratch
+    double* glue = nullptr;         // K5 potential refinement scratch
     long long xoff_n = 0;
     // host bookkeeping
     long long half_index = 0;
@@ -330,7 +331,7 @@ void free_all(dd_ctx* c) {
     }
     void* ptrs[] = {c->alphaA, c->alphaB, c->box, c->box2, c->off, c->off2, c->pool, c->scratch,
                     c->bump, c->lists, c->bside, c->slices[0], c->slices[1], c->counters, c->cellout, c->d_total, c->d_last, c->d_tot,
-                    c->eval_scratch, c->eval_res, c->d_sums, c->yacc, c->partial, c->d_xoff};
+                    c->eval_scratch, c->eval_res, c->d_sums, c->yacc, c->partial, c->d_xoff, c->glue};
     for (void* q : ptrs) if (q) cudaFree(q);
     for (auto& ev : c->pending) for (int k = 0; k < 3; ++k) cudaEventDestroy(ev.e[k]);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -634,6 +635,11 @@ int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, d
     CK(cudaMalloc(&c->d_sums, 4 * sizeof(double)));
     CK(cudaMalloc(&c->yacc, n2 * sizeof(unsigned long long)));
     CK(cudaMalloc(&c->partial, 256 * sizeof(double)));
+    {   // K5 scratch for the largest coarse layer
+        size_t g = 16;
+        for (int k = 0; k + 1 < nl; ++k) g = std::max(g, glue_scratch_doubles(c->L[k].side, c->L[k].s));
+        CK(cudaMalloc(&c->glue, g * sizeof(double)));
+    }
     CK(cudaMemsetAsync(c->d_last, 0, sizeof(DevStats), c->st));
     CK(cudaMemsetAsync(c->d_tot, 0, sizeof(DevStats), c->st));
     CK(cudaMemsetAsync(c->d_total, 0, 2 * sizeof(long long), c->st));
@@ -682,8 +688,17 @@ int dd_refine(dd_ctx* c) {
     std::swap(c->off, c->off2);
     std::swap(c->pool, c->scratch);
     const size_t n2 = (size_t)Lf.side * Lf.side;
-    CK(cudaMemsetAsync(c->alphaA, 0, n2 * sizeof(double), c->st));   // cold start (A14)
-    CK(cudaMemsetAsync(c->alphaB, 0, n2 * sizeof(double), c->st));
+    const bool striped = c->stripe_hi > c->stripe_lo;   // another rank owns part of alpha
+    if (c->opt.reserved[2] == 0 && !striped && c->last_part != 0) {
+        // glue the coarse potentials (Helmholtz least squares,
+        // P:1425-1452) and interpolate them in log space onto the fine layer
+        CK(launch_glue_refine(c->alphaA, c->alphaB, Lc.mu, Lc.side, Lc.s, c->eps, c->glue, c->alphaA, c->alphaB,
+                              c->st));
+        c->launches_pending += 4;
+    } else {
+        CK(cudaMemsetAsync(c->alphaA, 0, n2 * sizeof(double), c->st));   // cold start (reading A14)
+        CK(cudaMemsetAsync(c->alphaB, 0, n2 * sizeof(double), c->st));
+    }
     c->launches_pending += 3;
     c->cur += 1;
     c->stripe_lo = c->stripe_hi = 0;     // the driver sets the fine layer's stripe

@@ -47,6 +47,7 @@ struct K1Lay {
     float* XP;    // BIG: per-warp partial sums of the fused X2 LSE [warp][a_r a_c]
     float* FH;    // BIG: F (current) as separate hi / lo planes [a_r][a_c] for the Y1 pass
     float* FL;
+    float2* SXP;  // BIG: negated X2 stabilisers -(LM - F) for x1 pairs [a_r/2][a_c]
 };
 
 // BIG mode (fused Y2+X1): G is never stored as
@@ -74,17 +75,18 @@ __host__ __device__ inline void k1_sizes(int s, int bcap, size_t* sz, bool big =
     sz[12] = big ? (size_t)nwarps * A * A * 4 : 0;                  // XP
     sz[13] = big ? (size_t)A * A * 4 : 0;                            // FH
     sz[14] = big ? (size_t)A * A * 4 : 0;                            // FL
+    sz[15] = big ? (size_t)A * A * 4 : 0;                            // SXP
 }
 
 __host__ __device__ inline size_t k1_smem_bytes(int s, int bcap, bool big = false, int nwarps = 0) {
-    size_t sz[15], b = 0;
+    size_t sz[16], b = 0;
     k1_sizes(s, bcap, sz, big, nwarps);
-    for (int k = 0; k < 15; ++k) b += sz[k];
+    for (int k = 0; k < 16; ++k) b += sz[k];
     return b;
 }
 
 __device__ inline K1Lay k1_carve(unsigned char* base, int s, int bcap, bool big = false, int nwarps = 0) {
-    size_t sz[15];
+    size_t sz[16];
     k1_sizes(s, bcap, sz, big, nwarps);
     K1Lay L;
     size_t o = 0;
@@ -102,7 +104,8 @@ __device__ inline K1Lay k1_carve(unsigned char* base, int s, int bcap, bool big 
     L.CP = (float2*)(base + o); o += sz[11];
     L.XP = (float*)(base + o); o += sz[12];
     L.FH = (float*)(base + o); o += sz[13];
-    L.FL = (float*)(base + o);
+    L.FL = (float*)(base + o); o += sz[14];
+    L.SXP = (float2*)(base + o);
     return L;
 }
 
@@ -458,19 +461,9 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
     const int xi1 = lane % npair, xiq = lane / npair;
     const int x1a = 2 * xi1, x2q = 4 * xiq;
     const bool xvalid = x2q < d.ac;
-    float2 nSX[4], XA[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        XA[j] = make_float2(0.f, 0.f);
-        float sx0 = 0.f, sx1 = 0.f;
-        if (xvalid) {
-            const float2 f0 = Fcur[x1a * d.pX + x2q + j], f1 = Fcur[(x1a + 1) * d.pX + x2q + j];
-            const float l0 = L.LM[x1a * d.ac + x2q + j].x, l1 = L.LM[(x1a + 1) * d.ac + x2q + j].x;
-            if (f0.x > -INFINITY && l0 > -INFINITY) sx0 = l0 - f0.x;
-            if (f1.x > -INFINITY && l1 > -INFINITY) sx1 = l1 - f1.x;
-        }
-        nSX[j] = make_float2(-sx0, -sx1);
-    }
+    float* xp = L.XP + warp * (d.ar * d.ac);       // this warp's X2 partial sums (SMEM, zeroed here)
+    for (int o = lane; o < d.ar * d.ac; o += 32) xp[o] = 0.f;
+    __syncwarp();
     for (int grp = warp; grp < ngroups; grp += NT / 32) {
         const int y1b = grp * RG;
         const int y1B = y1b + rB;
@@ -532,6 +525,13 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
                     acc[i] = __fadd2_rn(acc[i], make_float2(ex2f(tt.x), ex2f(tt.y)));
                 }
             }
+            bool anybad = false;
+#pragma unroll
+            for (int r = 0; r < RG; ++r) {
+                const float s = (r & 1) ? acc[r >> 1].y : acc[r >> 1].x;
+                anybad |= ln[r].x != -INFINITY && (exact_all ? !(s > 0.f) : !(s >= 0.25f && s <= 4.0f));
+            }
+            anybad = __any_sync(0xffffffffu, anybad);
 #pragma unroll
             for (int r = 0; r < RG; ++r) {
                 float2 g = make_float2(-INFINITY, 0.f);
@@ -539,9 +539,9 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
                 float S = sp[r];
                 const bool live = ln[r].x != -INFINITY;
                 // exact recompute of an output whose speculative window failed
-                // (warp-uniform loop; rare after the first iterations of a solve)
-                const bool bad = live && (exact_all ? !(s > 0.f) : !(s >= 0.25f && s <= 4.0f));
-                if (__any_sync(0xffffffffu, bad)) {
+                // (rare after the first iterations of a solve)
+                if (anybad) {
+                    const bool bad = live && (exact_all ? !(s > 0.f) : !(s >= 0.25f && s <= 4.0f));
                     if (bad) {
                         float M = -INFINITY;
                         for (int x = 0; x < d.ar; ++x) M = fmaxf(M, Tc[x].x - cpb[x - r].x);
@@ -706,8 +706,14 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
         }
         __syncwarp();
         // fused X2: partial LSE over this group's rows, F_new(x1, x2) needs
-        // sum_y1 exp(U(y1, x2) - C(y1 - x1) - S(x1, x2))
+        // sum_y1 exp(U(y1, x2) - C(y1 - x1) - S(x1, x2)), S = LM - F (SXP pairs)
         if (xvalid) {
+            float2 XA[4], nSX[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                XA[j] = make_float2(xp[x1a * d.ac + x2q + j], xp[(x1a + 1) * d.ac + x2q + j]);
+                nSX[j] = L.SXP[xi1 * d.ac + x2q + j];
+            }
             for (int r = 0; r < RG && y1b + r < d.br; ++r) {
                 const int y1 = y1b + r;
                 const float2 cpr = CP[d.off + y1 - x1a];     // (C(x1a - y1), C(x1a + 1 - y1))
@@ -720,14 +726,6 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
                     XA[j] = __fadd2_rn(XA[j], make_float2(ex2f(t.x), ex2f(t.y)));
                 }
             }
-        }
-    }
-    // per-warp partials -> SMEM (every warp writes all of its slots)
-    {
-        float* xp = L.XP + warp * (d.ar * d.ac);
-        for (int o = lane; o < d.ar * d.ac; o += 32) xp[o] = 0.f;
-        __syncwarp();
-        if (xvalid) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 xp[x1a * d.ac + x2q + j] = XA[j].x;
@@ -848,6 +846,7 @@ __device__ void x2_finalize(const K1Lay& L, const Dims& d, const Grid& gq, const
             Fout[x1 * d.pX + x2] = make_float2(-INFINITY, 0.f);
             L.FH[o] = -INFINITY;
             L.FL[o] = 0.f;
+            reinterpret_cast<float*>(L.SXP)[((x1 >> 1) * d.ac + x2) * 2 + (x1 & 1)] = 0.f;
             continue;
         }
         float S = (fo.x > -INFINITY) ? lm.x - fo.x : 0.f;
@@ -873,6 +872,7 @@ __device__ void x2_finalize(const K1Lay& L, const Dims& d, const Grid& gq, const
             Fout[x1 * d.pX + x2] = make_float2(-INFINITY, 0.f);
             L.FH[o] = -INFINITY;
             L.FL[o] = 0.f;
+            reinterpret_cast<float*>(L.SXP)[((x1 >> 1) * d.ac + x2) * 2 + (x1 & 1)] = 0.f;
             continue;
         }
         float lh, ll;
@@ -881,6 +881,7 @@ __device__ void x2_finalize(const K1Lay& L, const Dims& d, const Grid& gq, const
         Fout[x1 * d.pX + x2] = fn;
         L.FH[o] = fn.x;
         L.FL[o] = fn.y;
+        reinterpret_cast<float*>(L.SXP)[((x1 >> 1) * d.ac + x2) * 2 + (x1 & 1)] = -(S + lh);   // next X2 stabiliser
         if (!(fabsf(fn.x) < 1e30f)) nonfinite = 1;
         // P_X pi(x) = mu(x) exp(F - F_new)  (plan (F, G))
         const float dF = (fo.x - fn.x) + (fo.y - fn.y) * kLN2;
@@ -1062,7 +1063,13 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
             lm = split_hl(p.logmu[g], gq);
         }
         L.FX[(x / d.ac) * d.pX + x % d.ac] = f;
-        if (BIG) { L.FH[x] = f.x; L.FL[x] = f.y; }
+        if (BIG) {
+            L.FH[x] = f.x;
+            L.FL[x] = f.y;
+            const int xl1 = x / d.ac, xl2 = x % d.ac;
+            reinterpret_cast<float*>(L.SXP)[((xl1 >> 1) * d.ac + xl2) * 2 + (xl1 & 1)] =
+                (f.x > -INFINITY && lm.x > -INFINITY) ? -(lm.x - f.x) : 0.f;
+        }
         L.LM[x] = lm;
         L.MU[x] = (float)m;
     }

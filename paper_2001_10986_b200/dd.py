@@ -122,7 +122,7 @@ class DD:
     def __init__(self, mu, nu, eps, cell_size, *, err_tol=1e-6, trunc_tau=1e-15,
                  max_inner_iter=10000, schedule=SCHED_FIXED, eps_start=0.0, coarsest_side=8,
                  no_truncate=False, device=0, pool_capacity=0, stream=None, device_input=False,
-                 bcap_main=0, bcap_big=0):
+                 bcap_main=0, bcap_big=0, cold_refine=False):
         opt = Options()
         opt.err_tol = err_tol
         opt.trunc_tau = trunc_tau
@@ -136,6 +136,7 @@ class DD:
         opt.stream = stream
         opt.reserved[0] = bcap_main
         opt.reserved[1] = bcap_big
+        opt.reserved[2] = 1 if cold_refine else 0
         self._h = C.c_void_p()
         if device_input:
             # mu, nu: objects exposing data_ptr() (device fp64) and a square shape

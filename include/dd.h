@@ -202,6 +202,13 @@ int dd_export_rows(dd_ctx* ctx, int row, int nrows, void* buf, size_t* bytes);
  * halo region (one boundary row at a time; DD_ENOMEM if it does not fit). */
 int dd_import_rows(dd_ctx* ctx, int row, int nrows, const void* buf, size_t bytes);
 
+/* dd_copy_alpha -- copy pixel rows [row0, row0+nrows) of the X-potential
+ * image alpha_A (partition 1) or alpha_B (2) of the current layer (fp64,
+ * cost units, row-major, side columns) to (to_ctx = 0) or from (to_ctx = 1)
+ * a caller DEVICE buffer.  The multi-GPU driver gathers the potentials of
+ * all stripes with it before dd_refine glues them. */
+int dd_copy_alpha(dd_ctx* ctx, int partition, int row0, int nrows, void* buf, int to_ctx);
+
 /* dd_y_accumulate -- add this context's sum_i nu_i(y) (2^60 fixed point,
  * deterministic) into a caller-zeroed DEVICE array acc[side*side] of uint64;
  * sum the arrays of all ranks (allreduce), then dd_y_l1 gives

@@ -875,6 +875,18 @@ int dd_import_rows(dd_ctx* c, int row, int nrows, const void* buf, size_t bytes)
     return DD_OK;
 }
 
+int dd_copy_alpha(dd_ctx* c, int partition, int row0, int nrows, void* buf, int to_ctx) {
+    if (!c || !buf || (partition != 1 && partition != 2)) return DD_EINVAL;
+    const Layer& Lr = c->L[c->cur];
+    if (row0 < 0 || nrows < 0 || row0 + nrows > Lr.side) { set_err(c, "alpha rows out of range"); return DD_EINVAL; }
+    double* a = (partition == 1 ? c->alphaA : c->alphaB) + (size_t)row0 * Lr.side;
+    const size_t bytes = (size_t)nrows * Lr.side * sizeof(double);
+    if (to_ctx) CK(cudaMemcpyAsync(a, buf, bytes, cudaMemcpyDeviceToDevice, c->st));
+    else CK(cudaMemcpyAsync(buf, a, bytes, cudaMemcpyDeviceToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return DD_OK;
+}
+
 int dd_y_accumulate(dd_ctx* c, unsigned long long* acc) {
     if (!c || !acc) return DD_EINVAL;
     const Layer& Lr = c->L[c->cur];

@@ -24,7 +24,7 @@ PLAN_BASIC_MARGINALS, PLAN_COO = 0, 1
 EXPORTS = ["dd_init", "dd_iterate", "dd_set_eps", "dd_refine", "dd_run_schedule", "dd_reset",
            "dd_primal_cost", "dd_marginal_error", "dd_fetch_plan", "dd_get_stats", "dd_get_totals",
            "dd_reset_totals", "dd_set_stripe", "dd_clear_rows", "dd_export_rows",
-           "dd_import_rows", "dd_y_accumulate", "dd_y_l1", "dd_phase_profile", "dd_get_cell_stats", "dd_get_state_info", "dd_get_state", "dd_set_state",
+           "dd_import_rows", "dd_copy_alpha", "dd_y_accumulate", "dd_y_l1", "dd_phase_profile", "dd_get_cell_stats", "dd_get_state_info", "dd_get_state", "dd_set_state",
            "dd_build_schedule", "dd_measure_mufu_peak", "dd_synchronize", "dd_free",
            "dd_last_error", "dd_version"]
 
@@ -82,6 +82,7 @@ def lib():
         L.dd_export_rows.argtypes = [p, i, i, p, C.POINTER(C.c_size_t)]
         L.dd_import_rows.argtypes = [p, i, i, p, C.c_size_t]
         L.dd_y_accumulate.argtypes = [p, p]
+        L.dd_copy_alpha.argtypes = [p, i, i, i, p, i]
         L.dd_y_l1.argtypes = [p, p, C.POINTER(d)]
         L.dd_get_state_info.argtypes = [p, C.POINTER(StateInfo)]
         L.dd_get_state.argtypes = [p, p, p, p, p, p]
@@ -241,6 +242,10 @@ class DD:
     def import_rows(self, row, nrows, dev_buf, nbytes):
         return self._check(lib().dd_import_rows(self._h, row, nrows, C.c_void_p(dev_buf.data_ptr()), nbytes),
                            "import_rows")
+
+    def copy_alpha(self, partition, row0, nrows, dev_buf, to_ctx):
+        return self._check(lib().dd_copy_alpha(self._h, partition, row0, nrows, C.c_void_p(dev_buf.data_ptr()),
+                                               1 if to_ctx else 0), "copy_alpha")
 
     def y_accumulate(self, dev_acc):
         return self._check(lib().dd_y_accumulate(self._h, C.c_void_p(dev_acc.data_ptr())), "y_accumulate")

@@ -170,8 +170,37 @@ class StripedRun:
         """Call after init / reset (coarsest layer) or after a refine."""
         self._layer()
 
+    def _gather_alpha(self):
+        """Every rank needs the potentials of the whole layer to glue them
+        (dd_refine): A-cell potentials come from the A-cell's owner,
+        B-cell potentials from the B-cell's owner (basic row r lies in B-cell
+        row (r + 1) // 2); one all-reduce per partition of a zero-padded image."""
+        import torch
+        info = self.ranks[0][1].state_info()
+        side, s, nb = info["side"], info["s"], info["nb"]
+        b = self.bounds
+        for part in (1, 2):
+            full = torch.zeros(side * side, dtype=torch.float64, device=self.device)
+            for r, dd in self.ranks:
+                if part == 1:
+                    rows = range(b[r], b[r + 1])
+                else:
+                    q0, q1 = owned_cell_rows(nb, 2, b[r], b[r + 1])
+                    rows = [x for q in range(q0, q1) for x in cell_basic_rows(nb, 2, q)]
+                r0, r1 = min(rows) * s, (max(rows) + 1) * s
+                seg = torch.empty((r1 - r0) * side, dtype=torch.float64, device=self.device)
+                dd.copy_alpha(part, r0, r1 - r0, seg, to_ctx=False)
+                full[r0 * side:r1 * side] += seg
+            full = self.tr.allreduce_sum(full)
+            for _, dd in self.ranks:
+                dd.copy_alpha(part, 0, side, full, to_ctx=True)
+
     def refine(self):
         prev = self.bounds
+        if prev is not None:
+            self._gather_alpha()
+            for _, dd in self.ranks:
+                dd.set_stripe(0, 0)          # alpha is now global: dd_refine glues it
         for _, dd in self.ranks:
             dd.refine()
         self._layer(prev)

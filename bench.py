@@ -274,16 +274,16 @@ def main():
     nominal = 148 * 16 * (clk["sm_max_mhz"] or 1965.0) * 1e6
     k1_ms = tot["solve_ms"]
     achieved = tot["mufu_ops"] / (k1_ms * 1e-3)
-    prof_traffic = None
-    try:
+    prof_traffic, traffic_unit = None, None
+    try:   # committed ncu capture (dram__bytes_read + write of K1 in one finest-layer sweep)
         pj = json.load(open(os.path.join(ROOT, "profiles", "k1_traffic.json")))
-        prof_traffic = pj.get("bytes_per_launch")
+        prof_traffic, traffic_unit = pj.get("bytes_per_launch"), pj.get("unit")
     except Exception:
         pass
     roofline = {"bound": "alu", "pipe": "MUFU/XU ex2+log (SFU)", "achieved": achieved / 1e12,
                 "peak": peak / 1e12, "unit": "Top/s", "frac": achieved / peak,
                 "peak_source": "measured ex2.approx microbenchmark on this B200 (dd_measure_mufu_peak)",
-                "peak_nominal": nominal / 1e12, "traffic": prof_traffic,
+                "peak_nominal": nominal / 1e12, "traffic": prof_traffic, "traffic_unit": traffic_unit,
                 "kernel": "k1_cell_solve", "kernel_share_of_step": k1_ms / my_ms,
                 "mufu_ops_per_step": tot["mufu_ops"] / args.steps}
 

@@ -48,6 +48,7 @@ struct K1Lay {
     float* FH;    // BIG: F (current) as separate hi / lo planes [a_r][a_c] for the Y1 pass
     float* FL;
     float2* SXP;  // BIG: negated X2 stabilisers -(LM - F) for x1 pairs [a_r/2][a_c]
+    int2* RI;     // BIG: per Y row, the columns [lo, hi] where nu_cell > 0 (lo > hi: empty)
 };
 
 // BIG mode (fused Y2+X1): G is never stored as
@@ -76,17 +77,18 @@ __host__ __device__ inline void k1_sizes(int s, int bcap, size_t* sz, bool big =
     sz[13] = big ? (size_t)A * A * 4 : 0;                            // FH
     sz[14] = big ? (size_t)A * A * 4 : 0;                            // FL
     sz[15] = big ? (size_t)A * A * 4 : 0;                            // SXP
+    sz[16] = big ? align16((size_t)(bcap + 1) * 8) : 0;             // RI
 }
 
 __host__ __device__ inline size_t k1_smem_bytes(int s, int bcap, bool big = false, int nwarps = 0) {
-    size_t sz[16], b = 0;
+    size_t sz[17], b = 0;
     k1_sizes(s, bcap, sz, big, nwarps);
-    for (int k = 0; k < 16; ++k) b += sz[k];
+    for (int k = 0; k < 17; ++k) b += sz[k];
     return b;
 }
 
 __device__ inline K1Lay k1_carve(unsigned char* base, int s, int bcap, bool big = false, int nwarps = 0) {
-    size_t sz[16];
+    size_t sz[17];
     k1_sizes(s, bcap, sz, big, nwarps);
     K1Lay L;
     size_t o = 0;
@@ -105,7 +107,8 @@ __device__ inline K1Lay k1_carve(unsigned char* base, int s, int bcap, bool big 
     L.XP = (float*)(base + o); o += sz[12];
     L.FH = (float*)(base + o); o += sz[13];
     L.FL = (float*)(base + o); o += sz[14];
-    L.SXP = (float2*)(base + o);
+    L.SXP = (float2*)(base + o); o += sz[15];
+    L.RI = (int2*)(base + o);
     return L;
 }
 
@@ -468,13 +471,19 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
         const int y1b = grp * RG;
         const int y1B = y1b + rB;
         const bool rvalid = y1B < d.br;
+        // the group's non-zero column range [glo, ghi] (union of its rows)
+        int glo = 1 << 30, ghi = -1;
+#pragma unroll
+        for (int r = 0; r < RG; ++r)
+            if (y1b + r < d.br) { const int2 ri = L.RI[y1b + r]; glo = min(glo, ri.x); ghi = max(ghi, ri.y); }
+        const int gend = ghi + 1;                     // exclusive end
         const int cpo = d.off - y1b;        // CP[cpo + x - r] = (C(x - y1b - r), C(x - y1b - r - 1))
 
         // ---------------------------------------------------------- phase A
         auto phaseA = [&](int c0) {
             const int y2 = c0 + lane;
-            const bool vy = y2 < d.bc;
-            const int y2c = vy ? y2 : d.bc - 1;          // clamped: every lane runs the same code
+            const bool vy = y2 < gend;
+            const int y2c = vy ? y2 : gend - 1;          // clamped: every lane runs the same code
             float2 ln[RG];
             float sp[RG];
 #pragma unroll
@@ -575,7 +584,7 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
         // ---------------------------------------------------------- phase B
         auto phaseB = [&](int c0, bool maxmode, const float* S, float* A) {
             const int ybase = c0 + hB * SUB;
-            const int nk = min(SUB, d.bc - ybase);
+            const int nk = min(SUB, gend - ybase);
             const float2* __restrict__ gp = gb + rB * PR + hB * (SUB + 1);
             // pair table: cp[k] = (C(y2 - x2b), C(y2 - x2b - 1)), y2 = ybase + k; cp[k - 2] the next two
             const float2* __restrict__ cp = CP + d.off + ybase - x2b;
@@ -656,13 +665,13 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
             float A[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) A[j] = maxmode ? -INFINITY : 0.f;
-            for (int c0 = 0; c0 < d.bc; c0 += 32) {
+            for (int c0 = glo; c0 < gend; c0 += 32) {
                 if (!a_done) phaseA(c0);
                 __syncwarp();
                 phaseB(c0, maxmode, S, A);
                 __syncwarp();
             }
-            a_done = (d.bc <= 32);
+            a_done = (gend - glo <= 32);
 #pragma unroll
             for (int j = 0; j < 4; ++j)
                 for (int o = YS >> 1; o > 0; o >>= 1) {
@@ -1098,6 +1107,21 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         npos += (v > 0.0) ? 1.0 : 0.0;
     }
     npos = block_sum(npos, L.red);     // (barrier: staging complete)
+    if (BIG) {
+        // per Y row: the non-zero columns of nu_cell.  The separable passes
+        // only need those (G = -inf elsewhere); about half of a union box is
+        // zero (basic-cell supports are bands inside their bounding boxes).
+        const int lane = tid & 31;
+        for (int r = tid >> 5; r < d.br; r += NT / 32) {
+            int lo = 1 << 30, hi = -1;
+            for (int c = lane; c < d.bc; c += 32)
+                if (LNU[r * d.bc + c].x != -INFINITY) { lo = min(lo, c); hi = max(hi, c); }
+            lo = warp_min_i(lo);
+            hi = warp_max_i(hi);
+            if (lane == 0) L.RI[r] = make_int2(lo, hi);
+        }
+        __syncthreads();
+    }
 
     // ---- line 9: Sinkhorn (Y-iteration first; stop test fused in the X-iteration)
     const double tol = muJ * p.err_tol;
@@ -1160,7 +1184,9 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         // algorithmic MUFU ops: one ex2 per term of the four 1D
         // passes + one log per pass output; + the extraction Y-iteration
         const double ar = d.ar, ac = d.ac, br = d.br, bc = d.bc;
-        const double per_it = ar * ac * bc + ar * npos + br * bc * ac + ac * br * ar
+        // Y1 a_r a_c b_c + Y2 a_r n_y + X1 n_y a_c + X2 a_c b_r a_r exps (terms
+        // with nu_cell(y) = 0 are -inf and not algorithmic work) + one log per output
+        const double per_it = ar * ac * bc + ar * npos + npos * ac + ac * br * ar
                               + ar * bc + npos + br * ac + ar * ac;
         co.mufu = per_it * it + (ar * ac * bc + ar * br * bc + ar * bc + br * bc);
     }

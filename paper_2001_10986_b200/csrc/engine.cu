@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -87,6 +88,7 @@ struct dd_ctx {
     long long halo_cap = 0;
     long long* d_xoff = nullptr;    // row export/import offsets scratch
     double* glue = nullptr;         // K5 potential refinement scratch
+    bool serial = false;            // DD_SERIAL_TIERS=1: all K1 tiers on one stream (profiling)
     long long xoff_n = 0;
     // host bookkeeping
     long long half_index = 0;
@@ -274,14 +276,14 @@ int sweep(dd_ctx* c) {
         q.bcap = c->bcap_big2;
         q.list_in = sorted + c->ncell_max; q.n_in = c->counters + 2; q.work_counter = c->counters + 5;
         q.gscratch = c->slices[1]; q.gslice = c->slice_bytes[1];
-        CK(launch_k1(q, 2, std::min(c->grid_t[1], ncells), c->smem_big2, c->st_t[1]));
+        CK(launch_k1(q, 2, std::min(c->grid_t[1], ncells), c->smem_big2, c->serial ? c->st : c->st_t[1]));
     }
     {   // tier 1: fused path, 256 threads, 2 CTAs/SM (LPT order)
         SweepParams q = p;
         q.bcap = c->bcap_big;
         q.list_in = sorted; q.n_in = c->counters + 1; q.work_counter = c->counters + 4;
         q.gscratch = c->slices[0]; q.gslice = c->slice_bytes[0];
-        CK(launch_k1(q, 1, std::min(c->grid_t[0], ncells), c->smem_big, c->st_t[0]));
+        CK(launch_k1(q, 1, std::min(c->grid_t[0], ncells), c->smem_big, c->serial ? c->st : c->st_t[0]));
     }
     {   // tier 0: the bulk, several CTAs per SM
         SweepParams q = p;
@@ -494,6 +496,10 @@ int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, d
         return DD_ECUDA;
     }
     c->grid_big = prop.multiProcessorCount;
+    {
+        const char* e = getenv("DD_SERIAL_TIERS");
+        c->serial = e && e[0] == '1';
+    }
     if (c->opt.stream) c->st = (cudaStream_t)c->opt.stream;
     else {
         CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));

@@ -528,8 +528,8 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
                 if (AR == 8) t.x = (x < d.ar) ? t.x : -INFINITY;     // s = 4 edge cells (a_r = 4)
 #pragma unroll
                 for (int i = 0; i < RG / 2; ++i) {
-                    float2 tt = __fadd2_rn(make_float2(t.x, t.x), neg2(cpb[x - 2 * i]));
-                    tt = __fadd2_rn(tt, nS[i]);
+                    const float2 cs = __fadd2_rn(cpb[x - 2 * i], neg2(nS[i]));   // C + S (exact)
+                    float2 tt = __fadd2_rn(make_float2(t.x, t.x), neg2(cs));
                     tt = __ffma2_rn(tt, L2E2, make_float2(t.y, t.y));
                     acc[i] = __fadd2_rn(acc[i], make_float2(ex2f(tt.x), ex2f(tt.y)));
                 }
@@ -600,11 +600,14 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
             const float2 nS01 = make_float2(-S[0], -S[1]), nS23 = make_float2(-S[2], -S[3]);
             float2 a01 = make_float2(A[0], A[1]), a23 = make_float2(A[2], A[3]);
             float2 b01 = make_float2(0.f, 0.f), b23 = make_float2(0.f, 0.f);   // second accumulator chain
+            // (C + S) first (exact on the hi grid, independent of G): one dependent
+            // FADD2 before the FFMA2, the same bits as (G - C) - S
+            const float2 S01 = neg2(nS01), S23 = neg2(nS23);
             auto body = [&](float2 g, float2 p01, float2 p23, float2& s01, float2& s23) {
-                float2 t01 = __fadd2_rn(make_float2(g.x, g.x), neg2(p01));
-                float2 t23 = __fadd2_rn(make_float2(g.x, g.x), neg2(p23));
-                t01 = __fadd2_rn(t01, nS01);
-                t23 = __fadd2_rn(t23, nS23);
+                const float2 cs01 = __fadd2_rn(p01, S01);
+                const float2 cs23 = __fadd2_rn(p23, S23);
+                float2 t01 = __fadd2_rn(make_float2(g.x, g.x), neg2(cs01));
+                float2 t23 = __fadd2_rn(make_float2(g.x, g.x), neg2(cs23));
                 t01 = __ffma2_rn(t01, L2E2, make_float2(g.y, g.y));
                 t23 = __ffma2_rn(t23, L2E2, make_float2(g.y, g.y));
                 s01 = __fadd2_rn(s01, make_float2(ex2f(t01.x), ex2f(t01.y)));

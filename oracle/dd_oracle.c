@@ -324,8 +324,10 @@ int ddo_init(ddo_ctx** out, int n, const double* mu, const double* nu, double ep
     c->eps = (c->opt.schedule == DDO_SCHED_LADDER) ? 2.0 / ((double)coarsest * coarsest) : eps;
     int rc = alloc_state(c);
     if (rc) { set_err(c, "out of memory"); return rc; }
-    rc = product_init(c);
-    if (rc) { set_err(c, "out of memory"); return rc; }
+    if (!c->opt.empty_init) {
+        rc = product_init(c);
+        if (rc) { set_err(c, "out of memory"); return rc; }
+    }
     c->half_index = 0;
     c->last_part = 0;
     return DDO_OK;
@@ -571,6 +573,22 @@ static int sweep(ddo_ctx* c) {
     free(rcs);
     if (rc == DDO_ENOCONV) set_err(c, "%d cells hit max_inner_iter", st.failed);
     if (rc == DDO_ENUMERIC) set_err(c, "non-finite marginal error in %d cells", st.failed);
+    return rc;
+}
+
+int ddo_solve_cells(ddo_ctx* c, int part, int n, const int* cells, int* iters) {
+    if (!c || (part != 1 && part != 2) || n < 0 || (n && !cells)) return DDO_EINVAL;
+    int nc = n_cells(c, part);
+    int rc = DDO_OK;
+    for (int k = 0; k < n; ++k) {
+        if (cells[k] < 0 || cells[k] >= nc) { set_err(c, "cell %d out of range", cells[k]); return DDO_EINVAL; }
+        cellres_t r;
+        memset(&r, 0, sizeof(r));
+        int s = solve_cell(c, part, cells[k], &r);
+        if (iters) iters[k] = r.iters;
+        if (s == DDO_ENOMEM) return s;
+        if (!rc && r.flag) rc = r.flag;
+    }
     return rc;
 }
 

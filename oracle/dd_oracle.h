@@ -40,6 +40,7 @@ typedef struct {
     double eps_start;      /* ladder: eps at the coarsest layer if > 2 h_0^2 (0 = none) */
     int coarsest_side;     /* ladder: coarsest layer side (0 -> 8) */
     int no_truncate;       /* 1 -> tau = 0 exactly (pins P3/P5) */
+    int empty_init;        /* 1 -> no product initialisation: empty state, a state is imported next */
 } ddo_options;
 
 typedef struct {
@@ -79,6 +80,12 @@ int ddo_init(ddo_ctx** out, int n, const double* mu, const double* nu, double ep
              int cell_size, const ddo_options* opt);
 int ddo_set_eps(ddo_ctx* c, double eps);
 int ddo_iterate(ddo_ctx* c, int n_half_iters);
+/* Algorithm 2 lines 8-13 for the listed composite cells of partition `part`
+ * only (1 = A, 2 = B; row-major cell index), on the current state; cells of
+ * one partition are disjoint, so this is exactly what a sweep does to them.
+ * Does not advance the half-iteration.  iters[k] receives each solve's
+ * Sinkhorn iteration count (may be NULL).  For sampled full-size parity. */
+int ddo_solve_cells(ddo_ctx* c, int part, int n, const int* cells, int* iters);
 int ddo_refine(ddo_ctx* c);
 int ddo_run_schedule(ddo_ctx* c);
 int ddo_primal_cost(ddo_ctx* c, double* transport_cost, double* entropic);

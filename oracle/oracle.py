@@ -31,7 +31,7 @@ class _Opt(C.Structure):
     _fields_ = [("err_tol", C.c_double), ("trunc_tau", C.c_double),
                 ("max_inner_iter", C.c_int), ("n_threads", C.c_int),
                 ("schedule", C.c_int), ("eps_start", C.c_double),
-                ("coarsest_side", C.c_int), ("no_truncate", C.c_int)]
+                ("coarsest_side", C.c_int), ("no_truncate", C.c_int), ("empty_init", C.c_int)]
 
 
 class _Stats(C.Structure):
@@ -61,6 +61,7 @@ def lib():
         _lib.ddo_init.argtypes = [C.POINTER(p), i, dp, dp, d, i, C.POINTER(_Opt)]
         _lib.ddo_set_eps.argtypes = [p, d]
         _lib.ddo_iterate.argtypes = [p, i]
+        _lib.ddo_solve_cells.argtypes = [p, i, i, p, p]
         _lib.ddo_refine.argtypes = [p]
         _lib.ddo_run_schedule.argtypes = [p]
         _lib.ddo_primal_cost.argtypes = [p, dp, dp]
@@ -111,12 +112,12 @@ class Oracle:
 
     def __init__(self, mu, nu, eps, cell_size, *, err_tol=1e-6, trunc_tau=1e-15,
                  max_inner_iter=10000, n_threads=0, schedule=SCHED_FIXED, eps_start=0.0,
-                 coarsest_side=8, no_truncate=False):
+                 coarsest_side=8, no_truncate=False, empty_init=False):
         self.mu = np.ascontiguousarray(mu, dtype=np.float64)
         self.nu = np.ascontiguousarray(nu, dtype=np.float64)
         n = self.mu.shape[0]
         opt = _Opt(err_tol, trunc_tau, max_inner_iter, n_threads, schedule, eps_start,
-                   coarsest_side, 1 if no_truncate else 0)
+                   coarsest_side, 1 if no_truncate else 0, 1 if empty_init else 0)
         self._h = C.c_void_p()
         rc = lib().ddo_init(C.byref(self._h), n, _dp(self.mu), _dp(self.nu), eps, cell_size,
                             C.byref(opt))
@@ -144,6 +145,14 @@ class Oracle:
 
     def iterate(self, k=1):
         return self._check(lib().ddo_iterate(self._h, k), "iterate", (OK, ENOCONV))
+
+    def solve_cells(self, part, cells):
+        """Algorithm 2 lines 8-13 for the listed cells of partition part only."""
+        cells = np.ascontiguousarray(cells, np.int32)
+        iters = np.zeros(max(cells.size, 1), np.int32)
+        self._check(lib().ddo_solve_cells(self._h, part, cells.size, cells.ctypes.data, iters.ctypes.data),
+                    "solve_cells", (OK, ENOCONV))
+        return iters[:cells.size]
 
     def refine(self):
         return self._check(lib().ddo_refine(self._h), "refine")

@@ -373,3 +373,13 @@ def test_validation_errors(case):
         mu = mu.copy(); mu[:4, :4] = 0; mu /= mu.sum()
     with pytest.raises(ValueError):
         Oracle(mu, nu, 1.0, s)
+
+
+def test_solve_cells_equals_sweep_subset():
+    """ddo_solve_cells on every cell of a partition reproduces ddo_iterate."""
+    mu, nu = config_images(1)
+    a = Oracle(mu, nu, 2 / 32**2, 4)
+    b = Oracle(mu, nu, 2 / 32**2, 4)
+    a.iterate(1)
+    b.solve_cells(1, np.arange(16))
+    assert np.array_equal(a.basic_marginals_dense(), b.basic_marginals_dense())

@@ -49,6 +49,8 @@ struct K1Lay {
     float* FL;
     float2* SXP;  // BIG: negated X2 stabilisers -(LM - F) for x1 pairs [a_r/2][a_c]
     int2* RI;     // BIG: per Y row, the columns [lo, hi] where nu_cell > 0 (lo > hi: empty)
+    int* GL;      // BIG: row groups of the fused pass listed per warp (static LPT balance)
+    int* GW;      // BIG: per-warp offsets into GL [nwarps + 1]
 };
 
 // BIG mode (fused Y2+X1): G is never stored as
@@ -78,17 +80,19 @@ __host__ __device__ inline void k1_sizes(int s, int bcap, size_t* sz, bool big =
     sz[14] = big ? (size_t)A * A * 4 : 0;                            // FL
     sz[15] = big ? (size_t)A * A * 4 : 0;                            // SXP
     sz[16] = big ? align16((size_t)(bcap + 1) * 8) : 0;             // RI
+    sz[17] = big ? align16((size_t)(bcap / 4 + 2) * 4) : 0;         // GL
+    sz[18] = big ? align16((size_t)(nwarps + 1) * 4) : 0;           // GW
 }
 
 __host__ __device__ inline size_t k1_smem_bytes(int s, int bcap, bool big = false, int nwarps = 0) {
-    size_t sz[17], b = 0;
+    size_t sz[19], b = 0;
     k1_sizes(s, bcap, sz, big, nwarps);
-    for (int k = 0; k < 17; ++k) b += sz[k];
+    for (int k = 0; k < 19; ++k) b += sz[k];
     return b;
 }
 
 __device__ inline K1Lay k1_carve(unsigned char* base, int s, int bcap, bool big = false, int nwarps = 0) {
-    size_t sz[17];
+    size_t sz[19];
     k1_sizes(s, bcap, sz, big, nwarps);
     K1Lay L;
     size_t o = 0;
@@ -108,7 +112,9 @@ __device__ inline K1Lay k1_carve(unsigned char* base, int s, int bcap, bool big 
     L.FH = (float*)(base + o); o += sz[13];
     L.FL = (float*)(base + o); o += sz[14];
     L.SXP = (float2*)(base + o); o += sz[15];
-    L.RI = (int2*)(base + o);
+    L.RI = (int2*)(base + o); o += sz[16];
+    L.GL = (int*)(base + o); o += sz[17];
+    L.GW = (int*)(base + o);
     return L;
 }
 
@@ -448,7 +454,6 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
     static_assert(RG * PR <= kGbufPerWarp, "gbuf");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float2* gb = L.gbuf + warp * kGbufPerWarp;
-    const int ngroups = (d.br + RG - 1) / RG;
     const int rB = lane / (NQ * YS);
     const int qB = (lane / YS) % NQ;
     const int hB = lane % YS;
@@ -467,7 +472,8 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
     float* xp = L.XP + warp * (d.ar * d.ac);       // this warp's X2 partial sums (SMEM, zeroed here)
     for (int o = lane; o < d.ar * d.ac; o += 32) xp[o] = 0.f;
     __syncwarp();
-    for (int grp = warp; grp < ngroups; grp += NT / 32) {
+    for (int gk = L.GW[warp]; gk < L.GW[warp + 1]; ++gk) {      // this warp's groups (LPT, static)
+        const int grp = L.GL[gk];
         const int y1b = grp * RG;
         const int y1B = y1b + rB;
         const bool rvalid = y1B < d.br;
@@ -1122,6 +1128,40 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
             lo = warp_min_i(lo);
             hi = warp_max_i(hi);
             if (lane == 0) L.RI[r] = make_int2(lo, hi);
+        }
+        __syncthreads();
+        // static LPT assignment of the 4-row groups to warps: a group costs
+        // about its non-zero column span (+ a fixed part); fixed for the whole
+        // solve (nu_cell does not change) and deterministic
+        if (tid == 0) {
+            constexpr int NW = NT / 32;
+            const int ng = (d.br + 3) / 4;
+            int* w = reinterpret_cast<int*>(L.gbuf);       // temp (gbuf is idle in the prologue)
+            int* own = w + ng;
+            for (int g = 0; g < ng; ++g) {
+                int lo = 1 << 30, hi = -1;
+                for (int r = 4 * g; r < min(4 * g + 4, d.br); ++r) { lo = min(lo, L.RI[r].x); hi = max(hi, L.RI[r].y); }
+                const int len = hi >= lo ? hi - lo + 1 : 0;
+                w[g] = ((len + 8) << 12) | g;              // weight high, group id low (ng < 4096)
+            }
+            for (int a = 1; a < ng; ++a) {                 // insertion sort, descending weight
+                const int v = w[a];
+                int b = a - 1;
+                while (b >= 0 && w[b] < v) { w[b + 1] = w[b]; --b; }
+                w[b + 1] = v;
+            }
+            int load[NW], pos[NW];
+            for (int k = 0; k < NW; ++k) { load[k] = 0; pos[k] = 0; }
+            for (int a = 0; a < ng; ++a) {                 // greedy: to the least-loaded warp
+                int best = 0;
+                for (int k = 1; k < NW; ++k) if (load[k] < load[best]) best = k;
+                load[best] += w[a] >> 12;
+                own[a] = best;
+                pos[best]++;
+            }
+            L.GW[0] = 0;
+            for (int k = 0; k < NW; ++k) { L.GW[k + 1] = L.GW[k] + pos[k]; pos[k] = L.GW[k]; }
+            for (int a = 0; a < ng; ++a) L.GL[pos[own[a]]++] = w[a] & 0xfff;
         }
         __syncthreads();
     }

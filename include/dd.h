@@ -145,6 +145,15 @@ int dd_reset(dd_ctx* ctx);
  * transport_cost = <c, pi>; entropic = eps (KL(pi|K) - ||K||). */
 int dd_primal_cost(dd_ctx* ctx, double* transport_cost, double* entropic);
 
+/* dd_dual_gap -- relative primal-dual gap of eq. RelPDGap:
+ * (KL(pi|K) - J(u_hat, v_hat)) / (KL(pi|K) - ||K||), pi as in
+ * dd_primal_cost; u_hat = the potentials of the current layer glued by the
+ * discrete Helmholtz least squares (reading A25), v_hat = the
+ * Y-iteration against u_hat over the whole grid (dense in x, two separable
+ * fp64 passes: O(n^3), a diagnostic).  primal = KL - ||K||, dual = J - ||K||.
+ * Needs the whole layer (no multi-GPU stripe). */
+int dd_dual_gap(dd_ctx* ctx, double* primal, double* dual, double* rel_gap);
+
 /* dd_marginal_error -- l1_x = sum_x |P_X pi(x) - mu(x)| of that plan;
  * l1_y = sum_y |sum_i nu_i(y) - nu(y)| (A18). */
 int dd_marginal_error(dd_ctx* ctx, double* l1_x, double* l1_y);

@@ -756,6 +756,164 @@ static int evaluate(ddo_ctx* c, double* cost, double* ent, double* l1x) {
     return rc;
 }
 
+
+/* ----------------------------------------------------- primal-dual gap -- */
+/* Relative primal-dual gap, eq. RelPDGap:
+ *   (KL(pi|K) - J(u, v)) / (KL(pi|K) - ||K||)
+ * pi = the primal iterate of reading A15; the dual candidate follows Sec. 6.3
+ * (P:1416-1456): the X-scalings u_{A,J} are glued by the discrete Helmholtz
+ * least squares on the graph of A-cells (edges through B-cells, weights
+ * log q of P:1431, sign of reading A25), u_hat = exp(V_J) u_{A,J}; v_hat is
+ * the Y-iteration against u_hat (Remark Sinkhorn P:272), so that
+ * int u_hat (x) v_hat dK = ||nu|| and, with eq. EntropicOTDualObjective P:250,
+ *   J - ||K|| = <log u_hat, mu> + <log v_hat, nu> - ||nu||.
+ * Dense fp64, plain CG (no shared code with the GPU path). */
+static double cg_dot(const double* a, const double* b, int n) {
+    ksum_t s = {0, 0};
+    for (int i = 0; i < n; ++i) ks_add(&s, a[i] * b[i]);
+    return ks_get(&s);
+}
+
+/* y = L x on the A-cell graph: for every B-cell and ordered pair of its
+ * member basic cells (i1, i2): (Lx)_{A(i1)} += x_{A(i1)} - x_{A(i2)}. */
+static void glue_matvec(int nb, const double* x, double* y) {
+    int na = nb / 2, nbc = nb / 2 + 1;
+    for (int p = 0; p < na * na; ++p) y[p] = 0.0;
+    for (int q1 = 0; q1 < nbc; ++q1)
+        for (int q2 = 0; q2 < nbc; ++q2) {
+            int mr[4], mc[4], m = 0;
+            for (int r = 2 * q1 - 1; r <= 2 * q1; ++r)
+                for (int cc = 2 * q2 - 1; cc <= 2 * q2; ++cc)
+                    if (r >= 0 && r < nb && cc >= 0 && cc < nb) { mr[m] = r; mc[m] = cc; ++m; }
+            for (int a = 0; a < m; ++a)
+                for (int b = 0; b < m; ++b) {
+                    if (a == b) continue;
+                    int pa = (mr[a] / 2) * na + mc[a] / 2, pb = (mr[b] / 2) * na + mc[b] / 2;
+                    y[pa] += x[pa] - x[pb];
+                }
+        }
+}
+
+int ddo_dual_gap(ddo_ctx* c, double* primal, double* dual, double* rel) {
+    if (!c) return DDO_EINVAL;
+    layer_t* L = &c->L[c->cur];
+    int side = L->side, s = L->s, nb = L->nb, na = nb / 2;
+    double eps = c->eps;
+    double ent = 0;
+    int rc = evaluate(c, NULL, &ent, NULL);
+    if (rc) return rc;
+    double P = ent / eps;                                  /* KL(pi|K) - ||K|| */
+    /* a_i = log avg_{X_i} exp((aA - aB)/eps) dmu, b_i = log avg exp((aB - aA)/eps) dmu */
+    int nbb = nb * nb;
+    double* ab = (double*)calloc((size_t)2 * nbb, sizeof(double));
+    int n = na * na;
+    double* V = (double*)calloc((size_t)(n > 0 ? n : 1) * 4, sizeof(double));
+    size_t n2 = (size_t)side * side;
+    double* ah = (double*)malloc(n2 * sizeof(double));
+    double* T = (double*)malloc(n2 * sizeof(double));
+    if (!ab || !V || !ah || !T) { free(ab); free(V); free(ah); free(T); return DDO_ENOMEM; }
+    for (int i = 0; i < nbb; ++i) {
+        int r0 = (i / nb) * s, c0 = (i % nb) * s;
+        double mp = -INFINITY, mn = -INFINITY, sm = 0;
+        for (int k = 0; k < s * s; ++k) {
+            size_t g = (size_t)(r0 + k / s) * side + (c0 + k % s);
+            if (L->mu[g] > 0) {
+                double d = (c->alphaA[g] - c->alphaB[g]) / eps;
+                if (d > mp) mp = d;
+                if (-d > mn) mn = -d;
+            }
+        }
+        ksum_t sp = {0, 0}, sn = {0, 0};
+        for (int k = 0; k < s * s; ++k) {
+            size_t g = (size_t)(r0 + k / s) * side + (c0 + k % s);
+            if (L->mu[g] > 0) {
+                double d = (c->alphaA[g] - c->alphaB[g]) / eps;
+                ks_add(&sp, L->mu[g] * exp(d - mp));
+                ks_add(&sn, L->mu[g] * exp(-d - mn));
+                sm += L->mu[g];
+            }
+        }
+        ab[2 * i] = mp + log(ks_get(&sp) / sm);
+        ab[2 * i + 1] = mn + log(ks_get(&sn) / sm);
+    }
+    /* right-hand side: edge A(i1) -> A(i2) with log q = a_i1 + b_i2 asks
+     * V(A(i2)) - V(A(i1)) = log q; normal equations over both orientations */
+    double* R = V + n;
+    double* Pd = V + 2 * n;
+    double* AP = V + 3 * n;
+    for (int p = 0; p < n; ++p) R[p] = 0.0;
+    int nbc = nb / 2 + 1;
+    for (int q1 = 0; q1 < nbc; ++q1)
+        for (int q2 = 0; q2 < nbc; ++q2) {
+            int mr[4], mc[4], m = 0;
+            for (int r = 2 * q1 - 1; r <= 2 * q1; ++r)
+                for (int cc = 2 * q2 - 1; cc <= 2 * q2; ++cc)
+                    if (r >= 0 && r < nb && cc >= 0 && cc < nb) { mr[m] = r; mc[m] = cc; ++m; }
+            for (int a = 0; a < m; ++a)
+                for (int b = 0; b < m; ++b) {
+                    if (a == b) continue;
+                    int i1 = mr[a] * nb + mc[a], i2 = mr[b] * nb + mc[b];
+                    int p1 = (mr[a] / 2) * na + mc[a] / 2;
+                    /* gradient of (V2 - V1 - w12)^2/2 + (V1 - V2 - w21)^2/2 w.r.t. V1 */
+                    R[p1] += 0.5 * ((ab[2 * i2] + ab[2 * i1 + 1]) - (ab[2 * i1] + ab[2 * i2 + 1]));
+                }
+        }
+    /* plain CG from V = 0 (R has zero sum: the system is consistent) */
+    for (int p = 0; p < n; ++p) { V[p] = 0.0; Pd[p] = R[p]; }
+    double rr = cg_dot(R, R, n), rr0 = rr;
+    for (int it = 0; it < 20 * n + 100 && rr > 1e-28 * rr0 && rr > 0; ++it) {
+        glue_matvec(nb, Pd, AP);
+        double pap = cg_dot(Pd, AP, n);
+        if (!(pap > 0)) break;
+        double al = rr / pap;
+        for (int p = 0; p < n; ++p) { V[p] += al * Pd[p]; R[p] -= al * AP[p]; }
+        double rn = cg_dot(R, R, n);
+        for (int p = 0; p < n; ++p) Pd[p] = R[p] + (rn / rr) * Pd[p];
+        rr = rn;
+    }
+    /* glued alpha_hat = alpha_A + eps V(A(x)) */
+    for (size_t g = 0; g < n2; ++g) {
+        int r = (int)(g / side), q = (int)(g % side);
+        ah[g] = c->alphaA[g] + eps * V[(r / s / 2) * na + (q / s / 2)];
+    }
+    /* Y-iteration against u_hat, dense (log v_hat below) */
+    ksum_t dsum = {0, 0};
+    for (size_t g = 0; g < n2; ++g)
+        if (L->mu[g] > 0) ks_add(&dsum, L->mu[g] * ah[g] / eps);
+    double h2 = 1.0 / ((double)side * side);
+#ifdef _OPENMP
+    int nt = c->opt.n_threads > 0 ? c->opt.n_threads : omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 16) num_threads(nt)
+#endif
+    for (long long y = 0; y < (long long)n2; ++y) {
+        if (!(L->nu[y] > 0)) { T[y] = 0.0; continue; }
+        int y1 = (int)(y / side), y2 = (int)(y % side);
+        double mx = -INFINITY;
+        for (size_t x = 0; x < n2; ++x) {
+            if (!(L->mu[x] > 0)) continue;
+            double d1 = (double)((int)(x / side) - y1), d2 = (double)((int)(x % side) - y2);
+            double t = ah[x] / eps + L->logmu[x] - (d1 * d1 + d2 * d2) * h2 / eps;
+            if (t > mx) mx = t;
+        }
+        double sm = 0;
+        for (size_t x = 0; x < n2; ++x) {
+            if (!(L->mu[x] > 0)) continue;
+            double d1 = (double)((int)(x / side) - y1), d2 = (double)((int)(x % side) - y2);
+            sm += exp(ah[x] / eps + L->logmu[x] - (d1 * d1 + d2 * d2) * h2 / eps - mx);
+        }
+        /* v_hat is the density w.r.t. nu (K = exp(-c/eps) mu nu):
+         * log v_hat(y) = -LSE_x(log u_hat + log mu - c/eps) */
+        T[y] = L->nu[y] * (-(mx + log(sm)) - 1.0);                     /* nu log v_hat - nu */
+    }
+    for (size_t y = 0; y < n2; ++y) ks_add(&dsum, T[y]);
+    double D = ks_get(&dsum);                                   /* J - ||K|| */
+    if (primal) *primal = P;
+    if (dual) *dual = D;
+    if (rel) *rel = (P - D) / P;
+    free(ab); free(V); free(ah); free(T);
+    return DDO_OK;
+}
+
 int ddo_primal_cost(ddo_ctx* c, double* transport_cost, double* entropic) {
     if (!c) return DDO_EINVAL;
     return evaluate(c, transport_cost, entropic, NULL);

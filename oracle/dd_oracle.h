@@ -85,6 +85,9 @@ int ddo_iterate(ddo_ctx* c, int n_half_iters);
  * one partition are disjoint, so this is exactly what a sweep does to them.
  * Does not advance the half-iteration.  iters[k] receives each solve's
  * Sinkhorn iteration count (may be NULL).  For sampled full-size parity. */
+/* Relative primal-dual gap, eq. RelPDGap, dual candidate glued
+ * as in Sec. 6.3: primal = KL(pi|K) - ||K||, dual = J(u_hat, v_hat) - ||K||. */
+int ddo_dual_gap(ddo_ctx* c, double* primal, double* dual, double* rel);
 int ddo_solve_cells(ddo_ctx* c, int part, int n, const int* cells, int* iters);
 int ddo_refine(ddo_ctx* c);
 int ddo_run_schedule(ddo_ctx* c);

@@ -62,6 +62,7 @@ def lib():
         _lib.ddo_set_eps.argtypes = [p, d]
         _lib.ddo_iterate.argtypes = [p, i]
         _lib.ddo_solve_cells.argtypes = [p, i, i, p, p]
+        _lib.ddo_dual_gap.argtypes = [p, dp, dp, dp]
         _lib.ddo_refine.argtypes = [p]
         _lib.ddo_run_schedule.argtypes = [p]
         _lib.ddo_primal_cost.argtypes = [p, dp, dp]
@@ -145,6 +146,12 @@ class Oracle:
 
     def iterate(self, k=1):
         return self._check(lib().ddo_iterate(self._h, k), "iterate", (OK, ENOCONV))
+
+    def dual_gap(self):
+        """(KL - ||K||, J - ||K||, relative PD gap) of eq. RelPDGap."""
+        a, b, r = C.c_double(), C.c_double(), C.c_double()
+        self._check(lib().ddo_dual_gap(self._h, C.byref(a), C.byref(b), C.byref(r)), "dual_gap")
+        return a.value, b.value, r.value
 
     def solve_cells(self, part, cells):
         """Algorithm 2 lines 8-13 for the listed cells of partition part only."""

@@ -67,6 +67,10 @@ cudaError_t launch_l1y(const unsigned long long* acc, const double* nu, int side
 cudaError_t launch_glue_refine(const double* aA_c, const double* aB_c, const double* mu_c, int side_c, int s_c,
                                double eps, double* scratch, double* aA_f, double* aB_f, cudaStream_t st);
 size_t glue_scratch_doubles(int side_c, int s_c);
+cudaError_t launch_glue_phi(const double* aA, const double* aB, const double* mu, int side, int s, double eps,
+                            double* scratch, double** phi_out);
+cudaError_t launch_dual_terms(const double* phi, const double* mu, const double* logmu, const double* nu, int n,
+                              double eps, double kappa, double* T, double* term, cudaStream_t st);
 cudaError_t launch_mufu_bench(float* out, int blocks, int threads, int iters, cudaStream_t st);
 
 }  // namespace dd

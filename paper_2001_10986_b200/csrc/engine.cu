@@ -966,6 +966,49 @@ int dd_primal_cost(dd_ctx* c, double* transport_cost, double* entropic) {
     return DD_OK;
 }
 
+int dd_dual_gap(dd_ctx* c, double* primal, double* dual, double* rel_gap) {
+    if (!c) return DD_EINVAL;
+    int rc = dd_synchronize(c);
+    if (rc) return rc;
+    if (c->stripe_hi > c->stripe_lo) { set_err(c, "dd_dual_gap needs the whole layer (no stripe)"); return DD_EINVAL; }
+    double s3[3];
+    rc = evaluate(c, s3, false, nullptr, nullptr, nullptr, nullptr);
+    if (rc) return rc;
+    Layer& Lr = c->L[c->cur];
+    const double P = s3[1] / c->eps;                     // KL(pi|K) - ||K|| (A15)
+    // glue at the current layer (k_glue.cu, default stream), then the dense
+    // Y-iteration against u_hat and the dual terms
+    CK(cudaStreamSynchronize(c->st));
+    const size_t gneed = glue_scratch_doubles(Lr.side, Lr.s);
+    double* g = nullptr;
+    CK(cudaMalloc(&g, gneed * sizeof(double)));
+    double* phi = nullptr;
+    CK(launch_glue_phi(c->alphaA, c->alphaB, Lr.mu, Lr.side, Lr.s, c->eps, g, &phi));
+    CK(cudaDeviceSynchronize());
+    const size_t n2 = (size_t)Lr.side * Lr.side;
+    double* T = nullptr;
+    CK(cudaMalloc(&T, 2 * n2 * sizeof(double)));
+    const double kappa = c->eps * (double)Lr.side * Lr.side;
+    CK(launch_dual_terms(phi, Lr.mu, Lr.logmu, Lr.nu, Lr.side, c->eps, kappa, T, T + n2, c->st));
+    // fixed-order sum of the n^2 terms
+    std::vector<double> h(n2);
+    CK(cudaMemcpyAsync(h.data(), T + n2, n2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    cudaFree(T);
+    cudaFree(g);
+    double D = 0.0, comp = 0.0;                              // Neumaier, host (n^2 doubles, once)
+    for (size_t k = 0; k < n2; ++k) {
+        const double t = D + h[k];
+        comp += (std::fabs(D) >= std::fabs(h[k])) ? (D - t) + h[k] : (h[k] - t) + D;
+        D = t;
+    }
+    D += comp;
+    if (primal) *primal = P;
+    if (dual) *dual = D;
+    if (rel_gap) *rel_gap = (P - D) / P;
+    return DD_OK;
+}
+
 int dd_marginal_error(dd_ctx* c, double* l1_x, double* l1_y) {
     if (!c) return DD_EINVAL;
     int rc = dd_synchronize(c);

@@ -219,6 +219,25 @@ cudaError_t launch_glue_refine(const double* aA_c, const double* aB_c, const dou
     return cudaGetLastError();
 }
 
+// glued potential of the current layer only (the PD-gap dual candidate)
+cudaError_t launch_glue_phi(const double* aA, const double* aB, const double* mu, int side, int s, double eps,
+                            double* scratch, double** phi_out) {
+    const int nb = side / s, na = nb / 2;
+    double* ab = scratch;
+    double* work = ab + 2 * (size_t)nb * nb;
+    double* epsV = work + 4 * (size_t)na * na;
+    double* phi = epsV + (size_t)na * na;
+    k_glue_ab<<<(nb * nb + 7) / 8, 256>>>(aA, aB, mu, side, s, nb, eps, ab);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_glue_cg<<<1, 1024>>>(ab, nb, eps, 20 * nb * nb + 100, 1e-14, work, epsV);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    const long long n2 = (long long)side * side;
+    k_glue_apply<<<(int)std::min<long long>((n2 + 255) / 256, 148 * 16), 256>>>(aA, epsV, side, s, phi);
+    *phi_out = phi;
+    return cudaGetLastError();
+}
+
 size_t glue_scratch_doubles(int side_c, int s_c) {
     const size_t nb = side_c / s_c, na = nb / 2;
     return 2 * nb * nb + 5 * na * na + (size_t)side_c * side_c;

@@ -22,7 +22,7 @@ PLAN_BASIC_MARGINALS, PLAN_COO = 0, 1
 
 # every symbol include/dd.h declares (checked by tests/test_abi.py)
 EXPORTS = ["dd_init", "dd_iterate", "dd_set_eps", "dd_refine", "dd_run_schedule", "dd_reset",
-           "dd_primal_cost", "dd_marginal_error", "dd_fetch_plan", "dd_get_stats", "dd_get_totals",
+           "dd_primal_cost", "dd_dual_gap", "dd_marginal_error", "dd_fetch_plan", "dd_get_stats", "dd_get_totals",
            "dd_reset_totals", "dd_set_stripe", "dd_clear_rows", "dd_export_rows",
            "dd_import_rows", "dd_copy_alpha", "dd_y_accumulate", "dd_y_l1", "dd_phase_profile", "dd_get_cell_stats", "dd_get_state_info", "dd_get_state", "dd_set_state",
            "dd_build_schedule", "dd_measure_mufu_peak", "dd_synchronize", "dd_free",
@@ -71,6 +71,7 @@ def lib():
         L.dd_reset.argtypes = [p]
         L.dd_primal_cost.argtypes = [p, C.POINTER(d), C.POINTER(d)]
         L.dd_marginal_error.argtypes = [p, C.POINTER(d), C.POINTER(d)]
+        L.dd_dual_gap.argtypes = [p, C.POINTER(d), C.POINTER(d), C.POINTER(d)]
         L.dd_fetch_plan.argtypes = [p, i, p, C.POINTER(C.c_size_t)]
         L.dd_get_stats.argtypes = [p, C.POINTER(SweepStats)]
         L.dd_get_totals.argtypes = [p, C.POINTER(SweepStats)]
@@ -199,6 +200,12 @@ class DD:
         a, b = C.c_double(), C.c_double()
         self._check(lib().dd_primal_cost(self._h, C.byref(a), C.byref(b)), "primal_cost")
         return a.value, b.value
+
+    def dual_gap(self):
+        """(KL - ||K||, J - ||K||, relative PD gap) of eq. RelPDGap."""
+        a, b, r = C.c_double(), C.c_double(), C.c_double()
+        self._check(lib().dd_dual_gap(self._h, C.byref(a), C.byref(b), C.byref(r)), "dual_gap")
+        return a.value, b.value, r.value
 
     def marginal_error(self):
         a, b = C.c_double(), C.c_double()

@@ -218,3 +218,33 @@ def test_big_tier_parity_s8(DD, bcap_big):
     assert lx <= 1e-6 and ly <= 1e-6, (lx, ly)
     Dg, Do = g.basic_marginals_dense(), o.basic_marginals_dense()
     assert np.abs(Dg - Do).sum() <= 1e-5
+
+
+@pytest.mark.parametrize("sweeps", [3, 12])
+def test_pd_gap_parity(DD, sweeps):
+    """Relative PD gap of eq. RelPDGap (f1): the oracle's state
+    imported into the GPU library gives the same primal score, glued dual
+    objective and gap (same state: only the evaluation arithmetic differs)."""
+    mu, nu = config_images(1)
+    eps = 2.0 / 32**2
+    o = Oracle(mu, nu, eps, 4, err_tol=1e-8)
+    o.iterate(sweeps)
+    Po, Do, ro = o.dual_gap()
+    g = DD(mu, nu, eps, 4, err_tol=1e-8)
+    g.set_state(o.get_state())
+    Pg, Dg, rg = g.dual_gap()
+    assert abs(Pg - Po) <= 1e-10 * abs(Po)
+    assert abs(Dg - Do) <= 1e-10 * abs(Do)
+    assert abs(rg - ro) <= 1e-9 + 1e-4 * abs(ro)
+    assert rg > -1e-8
+
+
+def test_pd_gap_after_ladder_cfg2(DD):
+    """After the cfg-2 ladder the glued dual candidate certifies the GPU
+    iterate: small non-negative relative PD gap (P:1713-1717 reports ~1e-4 at
+    Err = 1e-4; here Err = 1e-6)."""
+    mu, nu = config_images(2)
+    g = DD(mu, nu, 0.5 / 64**2, 4, schedule=1, err_tol=1e-6, eps_start=1.0, coarsest_side=16)
+    g.run_schedule()
+    P, D, rel = g.dual_gap()
+    assert -1e-7 < rel < 1e-3, rel

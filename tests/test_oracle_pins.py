@@ -383,3 +383,31 @@ def test_solve_cells_equals_sweep_subset():
     a.iterate(1)
     b.solve_cells(1, np.arange(16))
     assert np.array_equal(a.basic_marginals_dense(), b.basic_marginals_dense())
+
+
+# ------------------------------------------------------------- PD gap (f1) --
+def test_pd_gap_single_cell_is_zero():
+    """One A-cell covering X (n = 2s): the A-sweep IS the global problem and
+    gluing is trivial, so at Err -> 0 the relative PD gap of eq. RelPDGap
+     vanishes: J(u, v) = KL(pi|K) at the optimum (Prop. Duality
+    (iii), P:263-264)."""
+    m8, n8 = gaussian_mixture_image(8, 1, 1), gaussian_mixture_image(8, 2, 1)
+    o = Oracle(m8, n8, 2 / 64, 4, err_tol=1e-12, no_truncate=True)
+    o.iterate(1)
+    P, D, rel = o.dual_gap()
+    assert abs(rel) < 1e-10 and P > 0
+
+
+def test_pd_gap_weak_duality_and_convergence():
+    """Weak duality J <= KL (Prop. Duality (ii)) up to the iterate's
+    marginal error, and the gap -> 0 as the DD converges to the global
+    optimum (Thm 2): the glued dual candidate of Sec. 6.3."""
+    mu, nu = config_images(1)
+    o = Oracle(mu, nu, 2 / 32**2, 4, err_tol=1e-10, no_truncate=True)
+    gaps = []
+    for k in (2, 4, 14, 40):
+        o.iterate(k)
+        gaps.append(o.dual_gap()[2])
+    assert all(g > -1e-9 for g in gaps)
+    assert all(b < a for a, b in zip(gaps, gaps[1:]))
+    assert gaps[-1] < 1e-7

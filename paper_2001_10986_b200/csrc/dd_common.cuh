@@ -42,6 +42,7 @@ struct SweepParams {
     int mode;             // 0: one CTA per cell; 1: work list in SMEM; 2: work list in global scratch
     unsigned char* gscratch;    // mode 2: per-CTA slice of global memory replacing SMEM
     long long gslice;           // bytes per CTA slice
+    long long sl_off, acc_off;  // BIG: byte offsets of the stabiliser and extraction arrays in a slice
     int4* box;            // nb*nb (y0r, y0c, hr, hc), updated in place
     long long* off;       // nb*nb offsets (in: pool_in, out: scratch)
     const double* pool_in;

@@ -234,6 +234,15 @@ void choose_caps(dd_ctx* c, int s) {
     c->smem_big2 = k1_smem_bytes_host(s, c->bcap_big2, true, 16);
 }
 
+// BIG tiers: layout of a CTA's global slice for box side cap q.bcap:
+// log nu_cell (b^2 float2) | phase-A stabilisers (b^2 float) | extraction sums (b^2 float4)
+void slice_offsets(SweepParams& q) {
+    auto al = [](long long v) { return (v + 255) & ~255LL; };
+    const long long b2 = (long long)q.bcap * q.bcap;
+    q.sl_off = al(b2 * (long long)sizeof(float2));
+    q.acc_off = q.sl_off + al(b2 * (long long)sizeof(float));
+}
+
 // One sweep (Alg. 2 lines 6-14) over the partition selected by the parity of
 // the half-iteration index (line 7: odd l -> A).
 //   K0 classify cells by union Y-box side -> tier lists (big tiers LPT-sorted)
@@ -276,6 +285,7 @@ int sweep(dd_ctx* c) {
         q.bcap = c->bcap_big2;
         q.list_in = sorted + c->ncell_max; q.n_in = c->counters + 2; q.work_counter = c->counters + 5;
         q.gscratch = c->slices[1]; q.gslice = c->slice_bytes[1];
+        slice_offsets(q);
         CK(launch_k1(q, 2, std::min(c->grid_t[1], ncells), c->smem_big2, c->serial ? c->st : c->st_t[1]));
     }
     {   // tier 1: fused path, 256 threads, 2 CTAs/SM (LPT order)
@@ -283,6 +293,7 @@ int sweep(dd_ctx* c) {
         q.bcap = c->bcap_big;
         q.list_in = sorted; q.n_in = c->counters + 1; q.work_counter = c->counters + 4;
         q.gscratch = c->slices[0]; q.gslice = c->slice_bytes[0];
+        slice_offsets(q);
         CK(launch_k1(q, 1, std::min(c->grid_t[0], ncells), c->smem_big, c->serial ? c->st : c->st_t[0]));
     }
     {   // tier 0: the bulk, several CTAs per SM

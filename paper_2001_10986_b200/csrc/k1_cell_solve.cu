@@ -51,6 +51,7 @@ struct K1Lay {
     int2* RI;     // BIG: per Y row, the columns [lo, hi] where nu_cell > 0 (lo > hi: empty)
     int* GL;      // BIG: row groups of the fused pass listed per warp (static LPT balance)
     int* GW;      // BIG: per-warp offsets into GL [nwarps + 1]
+    int2* GI;     // BIG: per row group, the union of its rows' non-zero column ranges
 };
 
 // BIG mode (fused Y2+X1): G is never stored as
@@ -82,17 +83,18 @@ __host__ __device__ inline void k1_sizes(int s, int bcap, size_t* sz, bool big =
     sz[16] = big ? align16((size_t)(bcap + 1) * 8) : 0;             // RI
     sz[17] = big ? align16((size_t)(bcap / 4 + 2) * 4) : 0;         // GL
     sz[18] = big ? align16((size_t)(nwarps + 1) * 4) : 0;           // GW
+    sz[19] = big ? align16((size_t)(bcap / 4 + 2) * 8) : 0;         // GI
 }
 
 __host__ __device__ inline size_t k1_smem_bytes(int s, int bcap, bool big = false, int nwarps = 0) {
-    size_t sz[19], b = 0;
+    size_t sz[20], b = 0;
     k1_sizes(s, bcap, sz, big, nwarps);
-    for (int k = 0; k < 19; ++k) b += sz[k];
+    for (int k = 0; k < 20; ++k) b += sz[k];
     return b;
 }
 
 __device__ inline K1Lay k1_carve(unsigned char* base, int s, int bcap, bool big = false, int nwarps = 0) {
-    size_t sz[19];
+    size_t sz[20];
     k1_sizes(s, bcap, sz, big, nwarps);
     K1Lay L;
     size_t o = 0;
@@ -114,7 +116,8 @@ __device__ inline K1Lay k1_carve(unsigned char* base, int s, int bcap, bool big 
     L.SXP = (float2*)(base + o); o += sz[15];
     L.RI = (int2*)(base + o); o += sz[16];
     L.GL = (int*)(base + o); o += sz[17];
-    L.GW = (int*)(base + o);
+    L.GW = (int*)(base + o); o += sz[18];
+    L.GI = (int2*)(base + o);
     return L;
 }
 
@@ -478,11 +481,8 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
         const int y1B = y1b + rB;
         const bool rvalid = y1B < d.br;
         // the group's non-zero column range [glo, ghi] (union of its rows)
-        int glo = 1 << 30, ghi = -1;
-#pragma unroll
-        for (int r = 0; r < RG; ++r)
-            if (y1b + r < d.br) { const int2 ri = L.RI[y1b + r]; glo = min(glo, ri.x); ghi = max(ghi, ri.y); }
-        const int gend = ghi + 1;                     // exclusive end
+        const int2 gi = L.GI[grp];
+        const int glo = gi.x, gend = gi.y + 1;        // exclusive end
         const int cpo = d.off - y1b;        // CP[cpo + x - r] = (C(x - y1b - r), C(x - y1b - r - 1))
 
         // ---------------------------------------------------------- phase A
@@ -1095,10 +1095,9 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     // (BIG: log nu_cell and the extraction sums live in the CTA's global slice)
     float2* LNU = BIG ? reinterpret_cast<float2*>(gslice) : L.LNU;
     const size_t b2 = (size_t)p.bcap * p.bcap;
-    float* SLg = BIG ? reinterpret_cast<float*>(gslice + ((b2 * sizeof(float2) + 255) & ~(size_t)255)) : nullptr;
-    float4* ACCp = BIG ? reinterpret_cast<float4*>(gslice + ((b2 * sizeof(float2) + 255) & ~(size_t)255) +
-                                                   ((b2 * sizeof(float) + 255) & ~(size_t)255))
-                       : reinterpret_cast<float4*>(L.G);
+    (void)b2;
+    float* SLg = BIG ? reinterpret_cast<float*>(gslice + p.sl_off) : nullptr;
+    float4* ACCp = BIG ? reinterpret_cast<float4*>(gslice + p.acc_off) : reinterpret_cast<float4*>(L.G);
     const int ny = d.br * d.bc;
     double npos = 0.0;
     for (int y = tid; y < ny; y += NT) {
@@ -1142,6 +1141,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
                 int lo = 1 << 30, hi = -1;
                 for (int r = 4 * g; r < min(4 * g + 4, d.br); ++r) { lo = min(lo, L.RI[r].x); hi = max(hi, L.RI[r].y); }
                 const int len = hi >= lo ? hi - lo + 1 : 0;
+                L.GI[g] = make_int2(lo, hi);
                 w[g] = ((len + 8) << 12) | g;              // weight high, group id low (ng < 4096)
             }
             for (int a = 1; a < ng; ++a) {                 // insertion sort, descending weight

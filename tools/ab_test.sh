@@ -1,0 +1,4 @@
+# usage: bash tools/ab_test.sh A B  -> alternating timing runs of libdd_gpu_A.so / libdd_gpu_B.so on cfg 5
+for v in $1 $2 $1 $2; do
+DD_LIB=paper_2001_10986_b200/libdd_gpu_$v.so timeout 300 python tools/profile_sweep.py --cfg 5 --quiet > gpurun_out/ab_$v.log 2>&1; echo $v $(tail -1 gpurun_out/ab_$v.log | cut -c1-60)
+done

@@ -248,3 +248,39 @@ def test_pd_gap_after_ladder_cfg2(DD):
     g.run_schedule()
     P, D, rel = g.dual_gap()
     assert -1e-7 < rel < 1e-3, rel
+
+
+def test_paper_schedule_kappa_quarter(DD):
+    """The paper's own tail: +2 sweeps at eps = 0.25 dx^2 on the
+    finest layer ((n-2)*8+2 sweeps), on the GPU vs the oracle."""
+    n = 64
+    mu, nu = gaussian_mixture_image(n, 31, 3), gaussian_mixture_image(n, 32, 3)
+    eps = 0.25 / n**2
+    g = DD(mu, nu, eps, 4, schedule=1, coarsest_side=8)
+    o = Oracle(mu, nu, eps, 4, schedule=O_LADDER, coarsest_side=8)
+    g.run_schedule()
+    o.run_schedule()
+    assert g.state_info()["half_index"] == o.state_info()["half_index"] == (6 - 2) * 8 + 2
+    cg, _ = g.primal_cost()
+    co, _ = o.primal_cost()
+    assert abs(cg - co) <= 1e-5 * co, (cg, co)
+    lx, ly = g.marginal_error()
+    assert lx <= 1e-6 and ly <= 1e-6
+
+
+def test_ladder_s8_big_tiers_128(DD):
+    """cfg-4 recipe (s = 8, anisotropic mixtures) at 128^2 through the whole
+    ladder with every cell above 18 px on the fused big-cell tiers."""
+    n = 128
+    mu, nu = gaussian_mixture_image(n, 41, 4), gaussian_mixture_image(n, 42, 4)
+    eps = 0.5 / n**2
+    g = DD(mu, nu, eps, 8, schedule=1, coarsest_side=8, bcap_main=18)
+    o = Oracle(mu, nu, eps, 8, schedule=O_LADDER, coarsest_side=8)
+    g.run_schedule()
+    o.run_schedule()
+    assert g.totals()["big_cells"] > 0
+    cg, _ = g.primal_cost()
+    co, _ = o.primal_cost()
+    assert abs(cg - co) <= 1e-5 * co, (cg, co)
+    lx, ly = g.marginal_error()
+    assert lx <= 1e-6 and ly <= 1e-6

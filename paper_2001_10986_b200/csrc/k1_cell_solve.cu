@@ -715,7 +715,14 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
                 float2 u = make_float2(-INFINITY, 0.f);
                 if (!empty[j] && acc[j] > 1e-37f) {
                     float lh, ll;
-                    ln_split(acc[j], gq, lh, ll);
+                    if (acc[j] >= 0.25f && acc[j] <= 4.0f) {
+                        // the common (speculative) case: lg2.approx is within ~1e-7 here
+                        const float l2 = lg2f(acc[j]);
+                        lh = gridq(l2 * kLN2, gq);
+                        ll = fmaf(-lh, kL2E, l2);
+                    } else {
+                        ln_split(acc[j], gq, lh, ll);
+                    }
                     u = make_float2(S[j] + lh, ll);
                     if (!(fabsf(u.x) < 1e30f)) nonfinite = 1;
                 }

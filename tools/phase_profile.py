@@ -11,7 +11,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-PROF_SO = os.path.join(ROOT, "paper_2001_10986_b200", "libdd_gpu_prof.so")
+PROF_SO = os.environ.get("DD_PROF_LIB", os.path.join(ROOT, "paper_2001_10986_b200", "libdd_gpu_prof.so"))
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--cfg", type=int, default=5)

@@ -8,6 +8,16 @@
 
 namespace dd {
 
+// K1 tier 1 (fused big-cell path): threads per CTA and resident CTAs per SM
+#ifndef DD_T1_NT
+#define DD_T1_NT 256
+#endif
+#ifndef DD_T1_MINB
+#define DD_T1_MINB 2
+#endif
+constexpr int kT1Threads = DD_T1_NT, kT1PerSM = DD_T1_MINB;
+
+
 // ------------------------------------------------------------ constants --
 constexpr float kL2E = 1.4426950408889634f;   // log2(e)
 constexpr float kLN2 = 0.6931471805599453f;

@@ -208,14 +208,15 @@ int check_overflow(dd_ctx* c) {
 //   tier 1 (BIG path, 256 threads, 2 CTAs/SM): <= bcap_big (<= kCap1);
 //   tier 2 (BIG path, 512 threads, 1 CTA/SM):  <= bcap_big2 (<= kCap2).
 constexpr int kCap1 = 120, kCap2 = 704;   // tier-1 cap 120: measured best split
-constexpr size_t kSmem1 = 110 * 1024, kSmem2 = 220 * 1024;
+// SMEM per CTA: 228 KB per SM shared by the resident CTAs, 1 KB reserved per CTA, ~1 KB static
+constexpr size_t kSmem1 = 233472 / kT1PerSM - 2048, kSmem2 = 220 * 1024;
 void tier_caps(int s, int opt_main, int opt_big, int* b0, int* b1, int* b2) {
     int want = (s <= 4) ? 32 : 24;   // measured: the fused path wins above ~24 px (s = 8)
     if (opt_main > 0) want = opt_main;
     if (want < 2 * s + 2) want = 2 * s + 2;
     *b0 = want;
     int big = want;
-    while (big < kCap1 && k1_smem_bytes_host(s, big + 1, true, 8) <= kSmem1) ++big;
+    while (big < kCap1 && k1_smem_bytes_host(s, big + 1, true, kT1Threads / 32) <= kSmem1) ++big;
     int big2 = big;
     if (opt_big > 0 && opt_big >= want && opt_big < big) big = opt_big;   // testing: force tier 2
     *b1 = big;
@@ -229,7 +230,7 @@ void choose_caps(dd_ctx* c, int s) {
     c->bcap_main = b0;
     c->smem_main = k1_smem_bytes_host(s, b0);
     c->bcap_big = std::min(b1, c->slice_cap[0]);
-    c->smem_big = k1_smem_bytes_host(s, c->bcap_big, true, 8);
+    c->smem_big = k1_smem_bytes_host(s, c->bcap_big, true, kT1Threads / 32);
     c->bcap_big2 = std::min(b2, c->slice_cap[1]);
     c->smem_big2 = k1_smem_bytes_host(s, c->bcap_big2, true, 16);
 }
@@ -631,7 +632,7 @@ int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, d
         c->slice_cap[0] = std::max(c->slice_cap[0], std::min(b1, c->L[k].side));
         c->slice_cap[1] = std::max(c->slice_cap[1], std::min(b2, c->L[k].side));
     }
-    c->grid_t[0] = 2 * prop.multiProcessorCount;
+    c->grid_t[0] = kT1PerSM * prop.multiProcessorCount;
     c->grid_t[1] = prop.multiProcessorCount;
     for (int t = 0; t < 2; ++t) {
         const long long b = c->slice_cap[t];

@@ -838,11 +838,16 @@ __device__ void y1_big(const K1Lay& L, const Dims& d, const Grid& gq, bool exact
 // xor-tree combine: deterministic); per row one LDS.64 of U and one of the
 // cost pair feed two exps.  An output whose sum leaves [1/4, 4] is recomputed
 // with an exact max over y1.  Accumulates the L1 X-error of the plan (F, G).
+template <int P>
+__device__ __forceinline__ void x2_out(const K1Lay& L, const Dims& d, const Grid& gq, int h, int x1a, int x2,
+                                       float2 lm0, float2 lm1, float2 fo0, float2 fo1, float S0, float S1,
+                                       float2 a, const float2* __restrict__ Ur, float2* Fout, double& err_acc,
+                                       int& fallbacks, int& nonfinite);
 template <int NT>
 __device__ void x2_finalize(const K1Lay& L, const Dims& d, const Grid& gq, const float2* Fcur, float2* Fout,
                             double& err_acc, int& fallbacks, int& nonfinite) {
     constexpr int P = NT / 128;
-    static_assert(P == 2 || P == 4, "x2 split");
+    static_assert(P == 1 || P == 2 || P == 4, "x2 split");
     if (threadIdx.x == 0) L.WK[0] = 0;     // unit counter of the next fused pass
     const int t = threadIdx.x / P, h = threadIdx.x % P;
     const int ntask = (d.ar >> 1) * d.ac;
@@ -877,7 +882,16 @@ __device__ void x2_finalize(const K1Lay& L, const Dims& d, const Grid& gq, const
         a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
     }
     if (!tv || h >= 2) return;
-    // lane h finalises output (x1a + h, x2)
+    // lane h finalises output (x1a + h, x2) (P = 1: both)
+    for (int hh = h; hh < 2; hh += (P == 1 ? 1 : 2)) x2_out<P>(L, d, gq, hh, x1a, x2, lm0, lm1, fo0, fo1, S0, S1, a,
+                                                             Ur, Fout, err_acc, fallbacks, nonfinite);
+}
+
+template <int P>
+__device__ __forceinline__ void x2_out(const K1Lay& L, const Dims& d, const Grid& gq, int h, int x1a, int x2,
+                                       float2 lm0, float2 lm1, float2 fo0, float2 fo1, float S0, float S1,
+                                       float2 a, const float2* __restrict__ Ur, float2* Fout, double& err_acc,
+                                       int& fallbacks, int& nonfinite) {
     const int x1 = x1a + h, o = x1 * d.ac + x2;
     const float2 lm = h ? lm1 : lm0;
     const float2 fo = h ? fo1 : fo0;
@@ -1511,7 +1525,7 @@ static cudaError_t launch_tier(const SweepParams& p, int grid, size_t smem, cuda
 // tier 1: BIG path, 256 threads, 2 CTAs/SM; tier 2: BIG path, 512 threads, 1 CTA/SM.
 cudaError_t launch_k1(const SweepParams& p, int tier, int grid, size_t smem, cudaStream_t st) {
     if (tier == 0) return launch_tier<256, false, 3>(p, grid, smem, st);
-    if (tier == 1) return launch_tier<256, true, 2>(p, grid, smem, st);
+    if (tier == 1) return launch_tier<kT1Threads, true, kT1PerSM>(p, grid, smem, st);
     return launch_tier<512, true, 1>(p, grid, smem, st);
 }
 

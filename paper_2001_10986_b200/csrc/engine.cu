@@ -295,7 +295,12 @@ int sweep(dd_ctx* c) {
         q.list_in = sorted; q.n_in = c->counters + 1; q.work_counter = c->counters + 4;
         q.gscratch = c->slices[0]; q.gslice = c->slice_bytes[0];
         slice_offsets(q);
-        CK(launch_k1(q, 1, std::min(c->grid_t[0], ncells), c->smem_big, c->serial ? c->st : c->st_t[0]));
+        const cudaError_t e1 = launch_k1(q, 1, std::min(c->grid_t[0], ncells), c->smem_big, c->serial ? c->st : c->st_t[0]);
+        if (e1 != cudaSuccess) {
+            set_err(c, "K1 tier 1 launch (grid %d, smem %zu, bcap %d): %s", std::min(c->grid_t[0], ncells),
+                    c->smem_big, q.bcap, cudaGetErrorString(e1));
+            return DD_ECUDA;
+        }
     }
     {   // tier 0: the bulk, several CTAs per SM
         SweepParams q = p;

@@ -437,7 +437,7 @@ __device__ __forceinline__ void lse_pass(const K1Lay& L, const Dims& d, const Gr
 //     broadcast and the cost pair (C(x1-y1), C(x1-y1-1)) one LDS.64 from the
 //     pair table CP; an output whose sum leaves [1/4, 4] is recomputed with
 //     an exact max (first iteration: exact two-pass for all).
-//   phase B (lane <-> (row r, x2 quad, y2 sub-slice)):
+//   phase B (lane <-> (row r, x2 quad, y2 slice hB: columns hB + YS k)):
 //     U(y1, x2) += sum_{y2 in chunk} exp(G(y1, y2) - C(y2 - x2) - S(y1, x2))
 //     (S = previous U; cost pairs slide with period 2 over y2; exact two-pass
 //     max on the first iteration or when the window check fails).
@@ -469,7 +469,10 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
     const int hB = lane % YS;
     const int x2b = 4 * qB;
     const bool qvalid = x2b < d.ac;       // NQ = 4 serves a_c = 16; NQ = 2 serves a_c = 8 and 4
-    const int gidxA = (lane / SUB) * (SUB + 1) + lane % SUB;   // phase-A write slot of this lane's y2
+    // phase-B lane hB owns the chunk columns hB, hB + YS, hB + 2 YS, ... (interleaved:
+    // the YS slices of an output get equal work on partial chunks and read
+    // conflict-free cost pairs); phase A stores column c at slot (c % YS, c / YS)
+    const int gidxA = (lane % YS) * (SUB + 1) + lane / YS;
     const float2 L2E2 = make_float2(kL2E, kL2E);
     const float2* CP = L.CP;
 
@@ -592,15 +595,16 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
 
         // ---------------------------------------------------------- phase B
         auto phaseB = [&](int c0, bool maxmode, const float* S, float* A) {
-            const int ybase = c0 + hB * SUB;
-            const int nk = min(SUB, gend - ybase);
+            const int yb0 = c0 + hB;                      // this lane's columns yb0 + YS k
+            const int nk = max(0, min(SUB, (gend - yb0 + YS - 1) / YS));
             const float2* __restrict__ gp = gb + rB * PR + hB * (SUB + 1);
-            // pair table: cp[k] = (C(y2 - x2b), C(y2 - x2b - 1)), y2 = ybase + k; cp[k - 2] the next two
-            const float2* __restrict__ cp = CP + d.off + ybase - x2b;
+            // pair table: cp[YS k] = (C(y2 - x2b), C(y2 - x2b - 1)), y2 = yb0 + YS k;
+            // cp[YS k - 2] the next two (x2b + 2, x2b + 3)
+            const float2* __restrict__ cp = CP + d.off + yb0 - x2b;
             if (maxmode) {
                 for (int k = 0; k < nk; ++k) {
                     const float gx = gp[k].x;
-                    const float2 p0 = cp[k], p1 = cp[k - 2];
+                    const float2 p0 = cp[YS * k], p1 = cp[YS * k - 2];
                     A[0] = fmaxf(A[0], gx - p0.x); A[1] = fmaxf(A[1], gx - p0.y);
                     A[2] = fmaxf(A[2], gx - p1.x); A[3] = fmaxf(A[3], gx - p1.y);
                 }
@@ -622,28 +626,37 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
                 s01 = __fadd2_rn(s01, make_float2(ex2f(t01.x), ex2f(t01.y)));
                 s23 = __fadd2_rn(s23, make_float2(ex2f(t23.x), ex2f(t23.y)));
             };
-            // cost pairs slide with period 2: the (j=2,3) pair at k is the (j=0,1) pair at k-2
-            float2 pa = cp[-2], pb = cp[-1];
             int k = 0;
-            for (; k + 4 <= nk; k += 4) {
-                const float2 p0 = cp[0], p1 = cp[1], p2 = cp[2], p3 = cp[3];
-                const float2 g0 = gp[0], g1 = gp[1], g2 = gp[2], g3 = gp[3];
-                body(g0, p0, pa, a01, a23);
-                body(g1, p1, pb, b01, b23);
-                body(g2, p2, p0, a01, a23);
-                body(g3, p3, p1, b01, b23);
-                pa = p2;
-                pb = p3;
-                gp += 4;
-                cp += 4;
-            }
-            for (; k < nk; ++k) {
-                const float2 p0 = cp[0];
-                body(gp[0], p0, pa, a01, a23);
-                pa = pb;
-                pb = p0;
-                ++gp;
-                ++cp;
+            if constexpr (YS == 2) {
+                // columns step by 2: the (j = 2, 3) pair at k is the (j = 0, 1) pair at k - 1
+                float2 pa = cp[-2];
+                for (; k + 4 <= nk; k += 4) {
+                    const float2 p0 = cp[0], p1 = cp[2], p2 = cp[4], p3 = cp[6];
+                    const float2 g0 = gp[0], g1 = gp[1], g2 = gp[2], g3 = gp[3];
+                    body(g0, p0, pa, a01, a23);
+                    body(g1, p1, p0, b01, b23);
+                    body(g2, p2, p1, a01, a23);
+                    body(g3, p3, p2, b01, b23);
+                    pa = p3;
+                    gp += 4;
+                    cp += 8;
+                }
+                for (; k < nk; ++k) {
+                    const float2 p0 = cp[0];
+                    body(gp[0], p0, pa, a01, a23);
+                    pa = p0;
+                    ++gp;
+                    cp += 2;
+                }
+            } else {
+                for (; k + 2 <= nk; k += 2) {
+                    const float2 g0 = gp[0], g1 = gp[1];
+                    body(g0, cp[0], cp[-2], a01, a23);
+                    body(g1, cp[YS], cp[YS - 2], b01, b23);
+                    gp += 2;
+                    cp += 2 * YS;
+                }
+                if (k < nk) body(gp[0], cp[0], cp[-2], a01, a23);
             }
             a01 = __fadd2_rn(a01, b01);
             a23 = __fadd2_rn(a23, b23);
@@ -1511,7 +1524,9 @@ cudaError_t launch_k0(const SweepParams& p, int b0, int b1, int* lists, int* cou
 template <int NT, bool BIG, int MINB>
 static cudaError_t launch_tier(const SweepParams& p, int grid, size_t smem, cudaStream_t st) {
     static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
+    // opt in whenever the request grows: the 48 KB default covers static +
+    // dynamic SMEM together, so a dynamic size just under 48 KB can fail too
+    if (smem > attr) {
         cudaError_t e = cudaFuncSetAttribute(k1_cell_solve<NT, BIG, MINB>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;

@@ -138,6 +138,17 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
     for (int k = 0; k < nw; ++k) t += red[k];
     return t;
 }
+// The same with one barrier: only valid when every thread's previous read of
+// red[] is separated from this call by at least one other block barrier.
+__device__ __forceinline__ double block_sum1(double v, double* red) {
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    const int nw = blockDim.x >> 5;
+    for (int k = 0; k < nw; ++k) t += red[k];
+    return t;
+}
 __device__ __forceinline__ double block_max(double v, double* red) {
     v = warp_max(v);
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;

@@ -1224,7 +1224,9 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         if (BIG) x2_finalize<NT>(L, d, gq, Fc, Fn, e_loc, fallbacks, nonfinite);
         else lse_pass<PX2, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
         PROF_T(tf);
-        err = block_sum(e_loc, L.red);      // includes the barrier
+        // one barrier: the previous iteration's reads of red[] are two
+        // barriers back (after Y1, after the Y2/X1 passes)
+        err = block_sum1(e_loc, L.red);
         PROF_T(tg);
         // per warp: busy time of the passes and barrier waits (phase profile build only)
         PROF_ADD(0, tb - ta); PROF_ADD(1, tc - tb); PROF_ADD(2, td - tc); PROF_ADD(3, te - td);

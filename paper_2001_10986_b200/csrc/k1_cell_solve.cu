@@ -453,6 +453,7 @@ __device__ __forceinline__ void lse_pass(const K1Lay& L, const Dims& d, const Gr
 // partial-sum combine, and fusing X2 into this pass, were both slower.)
 
 __device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
+template <bool B> struct BoolTag { static constexpr bool value = B; };
 
 template <int NT, int AR, int NQ, int RG>
 __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all,
@@ -472,7 +473,6 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
     // phase-B lane hB owns the chunk columns hB, hB + YS, hB + 2 YS, ... (interleaved:
     // the YS slices of an output get equal work on partial chunks and read
     // conflict-free cost pairs); phase A stores column c at slot (c % YS, c / YS)
-    const int gidxA = (lane % YS) * (SUB + 1) + lane / YS;
     const float2 L2E2 = make_float2(kL2E, kL2E);
     const float2* CP = L.CP;
 
@@ -492,45 +492,56 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
         const int cpo = d.off - y1b;        // CP[cpo + x - r] = (C(x - y1b - r), C(x - y1b - r - 1))
 
         // ---------------------------------------------------------- phase A
-        auto phaseA = [&](int c0) {
-            const int y2 = c0 + lane;
+        // Full chunk: lane <-> column c0 + lane, all RG rows (RG/2 row pairs).
+        // Half chunk (the group's last <= 16 columns; typical row bands are
+        // narrow): lane <-> (column c0 + lane % 16, row pair lane / 16), so no
+        // lane idles on the missing columns.
+        auto phaseA = [&](int c0, auto half_tag) {
+            constexpr bool H = decltype(half_tag)::value;
+            constexpr int NRL = H ? 2 : RG;             // rows per lane
+            constexpr int NP = NRL / 2;                 // row pairs per lane
+            const int cl = H ? (lane & 15) : lane;      // column within the chunk
+            const int rb = H ? 2 * (lane >> 4) : 0;     // first row of this lane
+            const int y2 = c0 + cl;
             const bool vy = y2 < gend;
             const int y2c = vy ? y2 : gend - 1;        // clamped: every lane runs the same code
-            float2 ln[RG];
-            float sp[RG];
+            float2 ln[NRL];
+            float sp[NRL];
 #pragma unroll
-            for (int r = 0; r < RG; ++r) {
+            for (int q = 0; q < NRL; ++q) {
+                const int r = rb + q;
                 const bool v = vy && (y1b + r < d.br);
                 const int idx = (y1b + r) * d.bc + y2;
-                ln[r] = v ? LNUg[idx] : make_float2(-INFINITY, 0.f);
-                sp[r] = v ? SLg[idx] : 0.f;
+                ln[q] = v ? LNUg[idx] : make_float2(-INFINITY, 0.f);
+                sp[q] = v ? SLg[idx] : 0.f;
             }
             const float2* __restrict__ Tc = L.Tt + y2c * d.pT;
-            const float2* __restrict__ cpb = CP + cpo;     // cpb[x - r] = (C(x-y1b-r), C(x-y1b-r-1))
+            // cpb[x - 2 i] = (C(x - r), C(x - r - 1)) for rows r = y1b + rb + 2 i, r + 1
+            const float2* __restrict__ cpb = CP + cpo - rb;
             if (exact_all) {
                 // exact two-pass: stabiliser = max_x1 (T.hi - C)
-                float2 M[RG / 2];
+                float2 M[NP];
 #pragma unroll
-                for (int i = 0; i < RG / 2; ++i) M[i] = make_float2(-INFINITY, -INFINITY);
+                for (int i = 0; i < NP; ++i) M[i] = make_float2(-INFINITY, -INFINITY);
 #pragma unroll 4
                 for (int x = 0; x < AR; ++x) {
                     float th = Tc[x].x;
                     if (AR == 8) th = (x < d.ar) ? th : -INFINITY;
 #pragma unroll
-                    for (int i = 0; i < RG / 2; ++i) {
+                    for (int i = 0; i < NP; ++i) {
                         const float2 tt = __fadd2_rn(make_float2(th, th), neg2(cpb[x - 2 * i]));
                         M[i] = make_float2(fmaxf(M[i].x, tt.x), fmaxf(M[i].y, tt.y));
                     }
                 }
 #pragma unroll
-                for (int i = 0; i < RG / 2; ++i) {
+                for (int i = 0; i < NP; ++i) {
                     sp[2 * i] = M[i].x > -INFINITY ? M[i].x : 0.f;
                     sp[2 * i + 1] = M[i].y > -INFINITY ? M[i].y : 0.f;
                 }
             }
-            float2 nS[RG / 2], acc[RG / 2];
+            float2 nS[NP], acc[NP];
 #pragma unroll
-            for (int i = 0; i < RG / 2; ++i) {
+            for (int i = 0; i < NP; ++i) {
                 nS[i] = make_float2(-sp[2 * i], -sp[2 * i + 1]);
                 acc[i] = make_float2(0.f, 0.f);
             }
@@ -539,7 +550,7 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
                 float2 t = Tc[x];
                 if (AR == 8) t.x = (x < d.ar) ? t.x : -INFINITY;     // s = 4 edge cells (a_r = 4)
 #pragma unroll
-                for (int i = 0; i < RG / 2; ++i) {
+                for (int i = 0; i < NP; ++i) {
                     const float2 cs = __fadd2_rn(cpb[x - 2 * i], neg2(nS[i]));   // C + S (exact)
                     float2 tt = __fadd2_rn(make_float2(t.x, t.x), neg2(cs));
                     tt = __ffma2_rn(tt, L2E2, make_float2(t.y, t.y));
@@ -548,29 +559,31 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
             }
             bool anybad = false;
 #pragma unroll
-            for (int r = 0; r < RG; ++r) {
-                const float s = (r & 1) ? acc[r >> 1].y : acc[r >> 1].x;
-                anybad |= ln[r].x != -INFINITY && (exact_all ? !(s > 0.f) : !(s >= 0.25f && s <= 4.0f));
+            for (int q = 0; q < NRL; ++q) {
+                const float s = (q & 1) ? acc[q >> 1].y : acc[q >> 1].x;
+                anybad |= ln[q].x != -INFINITY && (exact_all ? !(s > 0.f) : !(s >= 0.25f && s <= 4.0f));
             }
             anybad = __any_sync(0xffffffffu, anybad);
+            const int gslot = (cl % YS) * (SUB + 1) + cl / YS;
 #pragma unroll
-            for (int r = 0; r < RG; ++r) {
+            for (int q = 0; q < NRL; ++q) {
+                const int r = rb + q;
                 float2 g = make_float2(-INFINITY, 0.f);
-                float s = (r & 1) ? acc[r >> 1].y : acc[r >> 1].x;
-                float S = sp[r];
-                const bool live = ln[r].x != -INFINITY;
+                float s = (q & 1) ? acc[q >> 1].y : acc[q >> 1].x;
+                float S = sp[q];
+                const bool live = ln[q].x != -INFINITY;
                 // exact recompute of an output whose speculative window failed
                 // (rare after the first iterations of a solve)
                 if (anybad) {
                     const bool bad = live && (exact_all ? !(s > 0.f) : !(s >= 0.25f && s <= 4.0f));
                     if (bad) {
                         float M = -INFINITY;
-                        for (int x = 0; x < d.ar; ++x) M = fmaxf(M, Tc[x].x - cpb[x - r].x);
+                        for (int x = 0; x < d.ar; ++x) M = fmaxf(M, Tc[x].x - cpb[x - q].x);
                         s = 0.f;
                         if (M > -INFINITY)
                             for (int x = 0; x < d.ar; ++x) {
                                 const float2 t = Tc[x];
-                                s += ex2f(((t.x - cpb[x - r].x) - M) * kL2E + t.y);
+                                s += ex2f(((t.x - cpb[x - q].x) - M) * kL2E + t.y);
                             }
                         S = M;
                         if (!exact_all) ++fallbacks;
@@ -583,13 +596,13 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
                         const float ll2 = fmaf(-lh, kL2E, l2);
                         const float Sn = S + lh;
                         SLg[(y1b + r) * d.bc + y2] = Sn;
-                        g = make_float2(ln[r].x - Sn, ln[r].y - ll2);
+                        g = make_float2(ln[q].x - Sn, ln[q].y - ll2);
                         if (!(fabsf(Sn) < 1e30f)) nonfinite = 1;
                     } else {
                         nonfinite = 1;       // nu_cell(y) > 0 unreachable from X
                     }
                 }
-                gb[r * PR + gidxA] = g;
+                gb[r * PR + gslot] = g;
             }
         };
 
@@ -691,7 +704,10 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
 #pragma unroll
             for (int j = 0; j < 4; ++j) A[j] = maxmode ? -INFINITY : 0.f;
             for (int c0 = glo; c0 < gend; c0 += 32) {
-                if (!a_done) phaseA(c0);
+                if (!a_done) {
+                    if (gend - c0 <= 16) phaseA(c0, BoolTag<true>());
+                    else phaseA(c0, BoolTag<false>());
+                }
                 __syncwarp();
                 phaseB(c0, maxmode, S, A);
                 __syncwarp();

@@ -43,7 +43,8 @@ def span(c):
 
 
 nca = nb // 2 if part == 1 else nb // 2 + 1
-tot = dict(nz=0, rows=0, groups=0, chunks=0, cells=0, full=0)
+tot = dict(nz=0, rows=0, groups=0, chunks=0, half=0, cells=0, full=0)
+hist = np.zeros(8, np.int64)          # group union widths by 8-column bins (up to 64+)
 for cp in range(nca):
     r0, r1 = span(cp)
     for cq in range(nca):
@@ -80,7 +81,10 @@ for cp in range(nca):
             w = int(h[ok].max() - l[ok].min() + 1)
             tot["groups"] += 4 * w
             tot["chunks"] += 4 * 32 * ((w + 31) // 32)
+            tot["half"] += 4 * 32 * (w // 32) + (4 * 32 if w % 32 > 16 else (4 * 16 if w % 32 else 0))
+            hist[min(w // 8, 7)] += 1
         tot["cells"] += 1
 print("partition", part, "fused-tier cells", tot["cells"])
-for k in ("full", "rows", "groups", "chunks"):
+print("group widths (8-col bins):", hist.tolist())
+for k in ("full", "rows", "groups", "chunks", "half"):
     print(f"{k:7s} / nz = {tot[k] / tot['nz']:.3f}")

@@ -13,7 +13,7 @@ namespace dd {
 #define DD_T1_NT 256
 #endif
 #ifndef DD_T1_MINB
-#define DD_T1_MINB 2
+#define DD_T1_MINB 3
 #endif
 constexpr int kT1Threads = DD_T1_NT, kT1PerSM = DD_T1_MINB;
 

@@ -205,9 +205,12 @@ int check_overflow(dd_ctx* c) {
 
 // Box-side capacities of the three K1 tiers for basic cell side s:
 //   tier 0 (SMEM path, 256 threads, 3 CTAs/SM): union Y box <= bcap_main;
-//   tier 1 (BIG path, 256 threads, 2 CTAs/SM): <= bcap_big (<= kCap1);
+//   tier 1 (BIG path, kT1Threads = 256 threads, kT1PerSM = 3 CTAs/SM, <= 80 regs): <= bcap_big (<= kCap1);
 //   tier 2 (BIG path, 512 threads, 1 CTA/SM):  <= bcap_big2 (<= kCap2).
-constexpr int kCap1 = 120, kCap2 = 704;   // tier-1 cap 120: measured best split
+#ifndef DD_T1_CAP
+#define DD_T1_CAP 120
+#endif
+constexpr int kCap1 = DD_T1_CAP, kCap2 = 704;   // tier-1 cap: measured best split
 // SMEM per CTA: 228 KB per SM shared by the resident CTAs, 1 KB reserved per CTA, ~1 KB static
 constexpr size_t kSmem1 = 233472 / kT1PerSM - 2048, kSmem2 = 220 * 1024;
 void tier_caps(int s, int opt_main, int opt_big, int* b0, int* b1, int* b2) {
@@ -289,7 +292,7 @@ int sweep(dd_ctx* c) {
         slice_offsets(q);
         CK(launch_k1(q, 2, std::min(c->grid_t[1], ncells), c->smem_big2, c->serial ? c->st : c->st_t[1]));
     }
-    {   // tier 1: fused path, 256 threads, 2 CTAs/SM (LPT order)
+    {   // tier 1: fused path, 256 threads, 3 CTAs/SM (LPT order)
         SweepParams q = p;
         q.bcap = c->bcap_big;
         q.list_in = sorted; q.n_in = c->counters + 1; q.work_counter = c->counters + 4;

@@ -1555,7 +1555,7 @@ static cudaError_t launch_tier(const SweepParams& p, int grid, size_t smem, cuda
 }
 
 // tier 0: 256 threads, all arrays in SMEM, 3 CTAs/SM;
-// tier 1: BIG path, 256 threads, 2 CTAs/SM; tier 2: BIG path, 512 threads, 1 CTA/SM.
+// tier 1: BIG path, 256 threads, 3 CTAs/SM (80 registers); tier 2: BIG path, 512 threads, 1 CTA/SM.
 cudaError_t launch_k1(const SweepParams& p, int tier, int grid, size_t smem, cudaStream_t st) {
     if (tier == 0) return launch_tier<256, false, 3>(p, grid, smem, st);
     if (tier == 1) return launch_tier<kT1Threads, true, kT1PerSM>(p, grid, smem, st);

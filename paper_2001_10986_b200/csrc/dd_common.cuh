@@ -16,6 +16,11 @@ namespace dd {
 #define DD_T1_MINB 3
 #endif
 constexpr int kT1Threads = DD_T1_NT, kT1PerSM = DD_T1_MINB;
+// K1 tier 2 (the largest boxes, 1 CTA/SM): threads per CTA
+#ifndef DD_T2_NT
+#define DD_T2_NT 768
+#endif
+constexpr int kT2Threads = DD_T2_NT;
 
 
 // ------------------------------------------------------------ constants --

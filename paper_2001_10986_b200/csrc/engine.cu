@@ -206,7 +206,7 @@ int check_overflow(dd_ctx* c) {
 // Box-side capacities of the three K1 tiers for basic cell side s:
 //   tier 0 (SMEM path, 256 threads, 3 CTAs/SM): union Y box <= bcap_main;
 //   tier 1 (BIG path, kT1Threads = 256 threads, kT1PerSM = 3 CTAs/SM, <= 80 regs): <= bcap_big (<= kCap1);
-//   tier 2 (BIG path, 512 threads, 1 CTA/SM):  <= bcap_big2 (<= kCap2).
+//   tier 2 (BIG path, kT2Threads = 768 threads, 1 CTA/SM, <= 80 regs): <= bcap_big2 (<= kCap2).
 #ifndef DD_T1_CAP
 #define DD_T1_CAP 120
 #endif
@@ -223,7 +223,7 @@ void tier_caps(int s, int opt_main, int opt_big, int* b0, int* b1, int* b2) {
     int big2 = big;
     if (opt_big > 0 && opt_big >= want && opt_big < big) big = opt_big;   // testing: force tier 2
     *b1 = big;
-    while (big2 < kCap2 && k1_smem_bytes_host(s, big2 + 1, true, 16) <= kSmem2) ++big2;
+    while (big2 < kCap2 && k1_smem_bytes_host(s, big2 + 1, true, kT2Threads / 32) <= kSmem2) ++big2;
     *b2 = big2;
 }
 
@@ -235,7 +235,7 @@ void choose_caps(dd_ctx* c, int s) {
     c->bcap_big = std::min(b1, c->slice_cap[0]);
     c->smem_big = k1_smem_bytes_host(s, c->bcap_big, true, kT1Threads / 32);
     c->bcap_big2 = std::min(b2, c->slice_cap[1]);
-    c->smem_big2 = k1_smem_bytes_host(s, c->bcap_big2, true, 16);
+    c->smem_big2 = k1_smem_bytes_host(s, c->bcap_big2, true, kT2Threads / 32);
 }
 
 // BIG tiers: layout of a CTA's global slice for box side cap q.bcap:
@@ -284,7 +284,7 @@ int sweep(dd_ctx* c) {
     CK(cudaEventRecord(c->ev_fork, c->st));
     CK(cudaStreamWaitEvent(c->st_t[0], c->ev_fork, 0));
     CK(cudaStreamWaitEvent(c->st_t[1], c->ev_fork, 0));
-    {   // tier 2: the largest boxes (LPT order), fused path, 512 threads, 1 CTA/SM
+    {   // tier 2: the largest boxes (LPT order), fused path, 768 threads, 1 CTA/SM
         SweepParams q = p;
         q.bcap = c->bcap_big2;
         q.list_in = sorted + c->ncell_max; q.n_in = c->counters + 2; q.work_counter = c->counters + 5;

@@ -26,6 +26,9 @@
 // than threads, G lanes split the k-range of a task (shuffle-combined).
 #include "dd_common.cuh"
 
+#ifndef DD_T0_MINB
+#define DD_T0_MINB 3
+#endif
 namespace dd {
 
 constexpr int kR = 4;   // outputs per thread-task
@@ -55,7 +58,7 @@ struct K1Lay {
 // BIG mode (fused Y2+X1): G is never stored as
 // a b^2 array; log nu_cell (b^2 float2) and the extraction partial sums
 // (b^2 float4) live in an L2-resident global slice per CTA.
-constexpr int kGbufPerWarp = 288;   // max over (NQ, RG) of RG * YS * (SUB + 1)
+constexpr int kGbufPerWarp = 144;   // max over NQ (RG = 4) of RG * YS * (SUB + 1)
 
 __host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
 __host__ __device__ inline int k1_ct_off(int s, int bcap) { return (2 * s > bcap ? 2 * s : bcap) + 24; }
@@ -875,7 +878,8 @@ __device__ __forceinline__ void x2_out(const K1Lay& L, const Dims& d, const Grid
 template <int NT>
 __device__ void x2_finalize(const K1Lay& L, const Dims& d, const Grid& gq, const float2* Fcur, float2* Fout,
                             double& err_acc, int& fallbacks, int& nonfinite) {
-    constexpr int P = NT / 128;
+    // threads per task (power of two, <= 4; with NT = 768 the last 256 threads idle here)
+    constexpr int P = NT >= 512 ? 4 : NT / 128;
     static_assert(P == 1 || P == 2 || P == 4, "x2 split");
     if (threadIdx.x == 0) L.WK[0] = 0;     // unit counter of the next fused pass
     const int t = threadIdx.x / P, h = threadIdx.x % P;
@@ -1555,11 +1559,11 @@ static cudaError_t launch_tier(const SweepParams& p, int grid, size_t smem, cuda
 }
 
 // tier 0: 256 threads, all arrays in SMEM, 3 CTAs/SM;
-// tier 1: BIG path, 256 threads, 3 CTAs/SM (80 registers); tier 2: BIG path, 512 threads, 1 CTA/SM.
+// tier 1: BIG path, 256 threads, 3 CTAs/SM; tier 2: BIG path, 768 threads, 1 CTA/SM (both <= 80 registers).
 cudaError_t launch_k1(const SweepParams& p, int tier, int grid, size_t smem, cudaStream_t st) {
-    if (tier == 0) return launch_tier<256, false, 3>(p, grid, smem, st);
+    if (tier == 0) return launch_tier<256, false, DD_T0_MINB>(p, grid, smem, st);
     if (tier == 1) return launch_tier<kT1Threads, true, kT1PerSM>(p, grid, smem, st);
-    return launch_tier<512, true, 1>(p, grid, smem, st);
+    return launch_tier<kT2Threads, true, 1>(p, grid, smem, st);
 }
 
 }  // namespace dd

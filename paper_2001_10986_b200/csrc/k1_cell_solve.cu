@@ -878,8 +878,9 @@ __device__ __forceinline__ void x2_out(const K1Lay& L, const Dims& d, const Grid
 template <int NT>
 __device__ void x2_finalize(const K1Lay& L, const Dims& d, const Grid& gq, const float2* Fcur, float2* Fout,
                             double& err_acc, int& fallbacks, int& nonfinite) {
-    // threads per task (power of two, <= 4; with NT = 768 the last 256 threads idle here)
-    constexpr int P = NT >= 512 ? 4 : NT / 128;
+    // threads per task: the largest power of two <= min(4, NT / 128) (with
+    // NT = 768 the last 256 threads idle here, with NT = 384 the last 128)
+    constexpr int P = NT >= 512 ? 4 : (NT >= 256 ? 2 : 1);
     static_assert(P == 1 || P == 2 || P == 4, "x2 split");
     if (threadIdx.x == 0) L.WK[0] = 0;     // unit counter of the next fused pass
     const int t = threadIdx.x / P, h = threadIdx.x % P;

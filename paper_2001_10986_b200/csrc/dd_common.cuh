@@ -75,6 +75,7 @@ struct SweepParams {
     int* n_out;
     int* work_counter;    // modes 1/2 dynamic work index
     int* overflow;        // set if scratch capacity exceeded
+    int* ipred;           // this partition's iteration counts of the previous sweep (work predictor for the LPT order)
 };
 
 // ------------------------------------------------------------- helpers --

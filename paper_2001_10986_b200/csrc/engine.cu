@@ -57,7 +57,9 @@ struct dd_ctx {
     // sweep plumbing
     unsigned long long* bump = nullptr;
     int* lists = nullptr;           // tier lists [3][ncell_max] (K0) + LPT-sorted tiers 1, 2 [2][ncell_max]
-    int* bside = nullptr;           // union Y-box side per cell (K0)
+    int* bside = nullptr;           // LPT sort key per cell (K0)
+    int* ipred = nullptr;           // [2][ncell_max] iterations of each cell's last solve, per partition
+    int ipred_layer = -1;           // layer the predictions belong to
     int* counters = nullptr;        // [0..2] tier counts, [3..5] work counters, [6] overflow
     unsigned char* slices[2] = {nullptr, nullptr};   // BIG tiers: per-CTA global slices (log nu_cell, ACC)
     long long slice_bytes[2] = {0, 0};
@@ -275,6 +277,12 @@ int sweep(dd_ctx* c) {
     p.mu = Lr.mu; p.logmu = Lr.logmu; p.mass_i = Lr.mass;
     p.out = c->cellout;
     p.overflow = c->counters + 6;
+    // work predictor for the LPT order (order only: results do not depend on it)
+    if (c->ipred_layer != c->cur) {
+        CK(cudaMemsetAsync(c->ipred, 0, (size_t)2 * c->ncell_max * sizeof(int), c->st));
+        c->ipred_layer = c->cur;
+    }
+    p.ipred = c->ipred + (size_t)(part - 1) * c->ncell_max;
     SweepEvents ev;
     int rc = alloc_events(c, ev);
     if (rc) return rc;
@@ -352,7 +360,7 @@ void free_all(dd_ctx* c) {
         cudaFree(c->L[k].mu); cudaFree(c->L[k].nu); cudaFree(c->L[k].logmu); cudaFree(c->L[k].mass);
     }
     void* ptrs[] = {c->alphaA, c->alphaB, c->box, c->box2, c->off, c->off2, c->pool, c->scratch,
-                    c->bump, c->lists, c->bside, c->slices[0], c->slices[1], c->counters, c->cellout, c->d_total, c->d_last, c->d_tot,
+                    c->bump, c->lists, c->bside, c->ipred, c->slices[0], c->slices[1], c->counters, c->cellout, c->d_total, c->d_last, c->d_tot,
                     c->eval_scratch, c->eval_res, c->d_sums, c->yacc, c->partial, c->d_xoff, c->glue};
     for (void* q : ptrs) if (q) cudaFree(q);
     for (auto& ev : c->pending) for (int k = 0; k < 3; ++k) cudaEventDestroy(ev.e[k]);
@@ -629,6 +637,7 @@ int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, d
     c->ncell_max = (nbmax / 2 + 1) * (nbmax / 2 + 1);
     CK(cudaMalloc(&c->lists, (size_t)5 * c->ncell_max * sizeof(int)));
     CK(cudaMalloc(&c->bside, (size_t)c->ncell_max * sizeof(int)));
+    CK(cudaMalloc(&c->ipred, (size_t)2 * c->ncell_max * sizeof(int)));
     CK(cudaMalloc(&c->counters, 8 * sizeof(int)));
     CK(cudaMemsetAsync(c->counters, 0, 8 * sizeof(int), c->st));
     // BIG tiers: one global slice per persistent CTA holding log nu_cell

@@ -1273,6 +1273,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     fallbacks = (int)block_sum((double)fallbacks, L.red + 32);
     co.flags |= s_flag;
     co.iters = it;
+    if (tid == 0 && p.ipred) p.ipred[cell] = it;
     co.err = (float)err;
     co.fallbacks = fallbacks;
     {
@@ -1494,11 +1495,16 @@ __global__ void k0_classify(SweepParams p, int b0, int b1, int* lists, int* coun
     const int tier = (bmax <= b0 || small_x) ? 0 : (bmax <= b1 ? 1 : 2);
     const int k = atomicAdd(&counts[tier], 1);
     lists[tier * ncap + k] = cell;
-    bside[cell] = bmax;
+    // LPT key ~ predicted solve time: box area x the cell's iteration count in
+    // this partition's previous sweep (1 before the first), log-binned
+    const int ip = p.ipred ? max(1, p.ipred[cell]) : 1;
+    const float w = (float)max(bmax, 1) * (float)max(bmax, 1) * (float)ip;
+    bside[cell] = min(1023, (int)(32.f * __log2f(w)));
 }
 
-// LPT order for the big tiers: counting sort of the tier-t list by box side,
-// descending (largest, slowest cells start first).  One block per tier.
+// LPT order for the big tiers: counting sort of the tier-t list by the K0
+// key (predicted work), descending: the slowest cells start first.  One
+// block per tier.
 __global__ void k0_sort(const int* lists, const int* counts, int ncap, const int* bside, int* sorted) {
     __shared__ int hist[1024];
     const int t = 1 + blockIdx.x;

@@ -298,7 +298,9 @@ def main():
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
-            ge = DD(mu_p.numpy(), nu_p.numpy(), eps, s, **kw)
+            # same stream as torch's current stream: NCCL completion (TorchTransport)
+            # is ordered against it, so the library never reads an unfinished receive
+            ge = DD(mu_p.numpy(), nu_p.numpy(), eps, s, stream=stream.cuda_stream, **kw)
             if run is not None:
                 re = StripedRun([(rank, ge)], world, TorchTransport(dist, rank, world, dev, staging=staging), device=dev)
                 solve(ge, re)

@@ -65,7 +65,10 @@ typedef struct {                /* zero-initialised fields take the defaults */
     double err_tol;             /* Err: cell stop when L1 X-error <= ||mu_J|| Err; 0 -> 1e-6 */
     double trunc_tau;           /* truncation threshold; 0 -> 1e-15, <0 -> 0 */
     int max_inner_iter;         /* Sinkhorn iterations per cell solve; 0 -> 10000 */
-    int check_every;            /* stop-test cadence; 0/1 -> every iteration (parity mode, A5) */
+    int check_every;            /* stop-test cadence k (A5): a cell stops at the first iteration
+                                   it with it % k == 0 and err <= ||mu_J|| Err; 0/1 -> every
+                                   iteration (parity mode).  The error itself is fused into the
+                                   X-iteration, so k > 1 only delays the stop. */
     int n_gpus;                 /* reserved for striping; 0/1 -> one GPU */
     int schedule;               /* DD_SCHED_FIXED | DD_SCHED_LADDER */
     double eps_start;           /* ladder: eps at the coarsest layer if > 2 h_0^2 (0 = none) */
@@ -73,10 +76,13 @@ typedef struct {                /* zero-initialised fields take the defaults */
     int no_truncate;            /* 1 -> tau = 0 */
     unsigned int flags;         /* DD_FLAG_* */
     int device;                 /* CUDA device ordinal */
-    long long pool_capacity;    /* nu_i pool entries per buffer; 0 -> 48 * N^2 + 2^20 */
+    long long pool_capacity;    /* nu_i pool entries per buffer; 0 -> 64 * N^2 + 2^22.  Each of
+                                   the two pool buffers holds this plus a halo region of
+                                   pool_capacity / 3 entries for imported multi-GPU boundary
+                                   rows (fp64: 2 * 4/3 * 8 B per entry in total) */
     void* stream;               /* cudaStream_t to use, or NULL */
     int reserved[8];            /* [0] > 0: box-side cap of the SMEM tier (tier 0);
-                                   [1] > 0: box-side cap of the 2-CTA/SM fused tier (tier 1);
+                                   [1] > 0: box-side cap of the 3-CTA/SM fused tier (tier 1);
                                    testing knobs that route cells to the other K1 tiers;
                                    [2] = 1: cold-start potentials at dd_refine (reading A14)
                                    instead of the glued + interpolated warm start */
@@ -119,7 +125,10 @@ typedef struct {
 int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, double eps,
             int cell_size, const dd_options* opt);
 
-/* dd_iterate -- n_half_iters sweeps A, B, A, ... (Alg. 2 lines 5-14). */
+/* dd_iterate -- n_half_iters sweeps A, B, A, ... (Alg. 2 lines 5-14).
+ * Asynchronous (enqueued on the context stream; no host wait per sweep).
+ * Cells that hit max_inner_iter (reading A6) are reported by the next
+ * dd_synchronize / dd_run_schedule as DD_ENOCONV. */
 int dd_iterate(dd_ctx* ctx, int n_half_iters);
 
 /* dd_set_eps -- change eps keeping alpha = eps log u constant. */
@@ -133,7 +142,9 @@ int dd_set_eps(dd_ctx* ctx, double eps);
 int dd_refine(dd_ctx* ctx);
 
 /* dd_run_schedule -- LADDER mode: run the whole schedule (refinements, eps
- * stages, sweeps) asynchronously on the context stream. */
+ * stages, sweeps) on the context stream, then wait once at the end: returns
+ * DD_ENOCONV if any cell hit max_inner_iter (A6; the state stays
+ * Y-feasible), DD_ENOMEM on a pool overflow. */
 int dd_run_schedule(dd_ctx* ctx);
 
 /* dd_reset -- return to the initial state (coarsest layer, product coupling). */
@@ -252,6 +263,9 @@ int dd_build_schedule(int n_final, int coarsest_side, double kappa_final, double
  * clock (MHz) the measurement ran at (roofline denominator). */
 int dd_measure_mufu_peak(int device, double* ops_per_s);
 
+/* dd_synchronize -- wait for the context's work.  DD_ENOMEM on a pool or
+ * box-size overflow; DD_ENOCONV if cells hit max_inner_iter since the last
+ * report (each failure is reported once; dd_reset_totals forgets them). */
 int dd_synchronize(dd_ctx* ctx);
 void dd_free(dd_ctx* ctx);
 const char* dd_last_error(const dd_ctx* ctx);

@@ -110,18 +110,36 @@ static double lse_row(int ny, const double* g, const double* Crow, double eps) {
     return m + eps * log(s);
 }
 
-int ddo_sinkhorn_dense(int nx, int ny, const double* a, const double* b, const double* C,
-                       double eps, double tol, int max_iter, double* f, double* g,
-                       int* iters, double* err) {
+/* The loop of P:1404-1411.  check_every = k (reading A5): the stop test is
+ * evaluated after every X-iteration and honoured when it % k == 0.  The two
+ * half-iterations are independent per output (y, resp. x), so when called
+ * outside a parallel region (a few large sampled cells) their outputs are
+ * computed by nt OpenMP threads; every output is the same serial sum, so the
+ * result does not depend on the thread count. */
+static int sinkhorn_dense_k(int nx, int ny, const double* a, const double* b, const double* C,
+                            double eps, double tol, int max_iter, int check_every, int nt,
+                            double* f, double* g, int* iters, double* err) {
     double* fn = (double*)malloc(sizeof(double) * (size_t)(nx > 0 ? nx : 1));
     if (!fn) return DDO_ENOMEM;
+    if (check_every < 1) check_every = 1;
+    int par = 0;
+#ifdef _OPENMP
+    par = !omp_in_parallel() && nt > 1 && (double)nx * (double)ny > 2e5;
+#endif
+    (void)nt;
     int it = 0, rc = DDO_ENOCONV;
     double e = INFINITY;
     while (1) {
         /* Y-iteration */
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) num_threads(nt) if (par)
+#endif
         for (int y = 0; y < ny; ++y)
             g[y] = (b[y] > 0.0) ? eps * log(b[y]) - lse_col(nx, ny, f, C, y, eps) : -INFINITY;
         /* X-iteration */
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) num_threads(nt) if (par)
+#endif
         for (int x = 0; x < nx; ++x)
             fn[x] = (a[x] > 0.0) ? eps * log(a[x]) - lse_row(ny, g, C + (size_t)x * ny, eps)
                                  : -INFINITY;
@@ -130,7 +148,7 @@ int ddo_sinkhorn_dense(int nx, int ny, const double* a, const double* b, const d
         for (int x = 0; x < nx; ++x)
             if (a[x] > 0.0) e += a[x] * fabs(expm1((f[x] - fn[x]) / eps));
         ++it;
-        if (e <= tol) { rc = DDO_OK; break; }
+        if (e <= tol && it % check_every == 0) { rc = DDO_OK; break; }
         if (it >= max_iter) { rc = DDO_ENOCONV; break; }
         memcpy(f, fn, sizeof(double) * (size_t)nx);
     }
@@ -139,6 +157,12 @@ int ddo_sinkhorn_dense(int nx, int ny, const double* a, const double* b, const d
     if (err) *err = e;
     if (!isfinite(e)) return DDO_ENUMERIC;
     return rc;
+}
+
+int ddo_sinkhorn_dense(int nx, int ny, const double* a, const double* b, const double* C,
+                       double eps, double tol, int max_iter, double* f, double* g,
+                       int* iters, double* err) {
+    return sinkhorn_dense_k(nx, ny, a, b, C, eps, tol, max_iter, 1, 1, f, g, iters, err);
 }
 
 /* -------------------------------------------------------------- schedule -- */
@@ -251,6 +275,7 @@ int ddo_init(ddo_ctx** out, int n, const double* mu, const double* nu, double ep
     if (opt) c->opt = *opt;
     if (c->opt.err_tol <= 0) c->opt.err_tol = 1e-6;
     if (c->opt.max_inner_iter <= 0) c->opt.max_inner_iter = 10000;
+    if (c->opt.check_every <= 0) c->opt.check_every = 1;
     c->tau = c->opt.trunc_tau == 0.0 ? 1e-15 : (c->opt.trunc_tau < 0 ? 0.0 : c->opt.trunc_tau);
     if (c->opt.no_truncate) c->tau = 0.0;
     *out = c;
@@ -476,8 +501,12 @@ static int solve_cell(ddo_ctx* c, int part, int cidx, cellres_t* res) {
     /* line 9: pi_cell, u_{C,J} <- Sinkhorn(mu_J, nu_cell, u_{C,J}) */
     int it = 0;
     double err = 0;
-    int src = ddo_sinkhorn_dense(P.nx, P.ny, P.a, P.b, P.C, c->eps, muJ * c->opt.err_tol,
-                                 c->opt.max_inner_iter, P.f, P.g, &it, &err);
+    int nt = 1;
+#ifdef _OPENMP
+    nt = c->opt.n_threads > 0 ? c->opt.n_threads : omp_get_max_threads();
+#endif
+    int src = sinkhorn_dense_k(P.nx, P.ny, P.a, P.b, P.C, c->eps, muJ * c->opt.err_tol,
+                               c->opt.max_inner_iter, c->opt.check_every, nt, P.f, P.g, &it, &err);
     res->iters = it; res->err = err; res->flag = src;
     /* line 10: nu_i <- P_Y(pi_cell restricted to X_i x Y) */
     double* nu_i[4];

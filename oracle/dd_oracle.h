@@ -41,6 +41,7 @@ typedef struct {
     int coarsest_side;     /* ladder: coarsest layer side (0 -> 8) */
     int no_truncate;       /* 1 -> tau = 0 exactly (pins P3/P5) */
     int empty_init;        /* 1 -> no product initialisation: empty state, a state is imported next */
+    int check_every;       /* stop-test cadence k (reading A5): stop at it % k == 0; 0 -> 1 */
 } ddo_options;
 
 typedef struct {

@@ -13,6 +13,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle_dd.so")
 _SRC = os.path.join(_HERE, "dd_oracle.c")
+_SHIM = os.path.join(_HERE, "dd_shim.c")       # the SURVEY 8(b) dd_* ABI over ddo_*
 
 SCHED_FIXED = 0
 SCHED_LADDER = 1
@@ -21,9 +22,10 @@ OK, EINVAL, ENOCONV, ENUMERIC, ENOMEM = 0, 1, 2, 3, 6
 
 def build_oracle(force: bool = False) -> str:
     """Compile the oracle (plain C11, fp64, OpenMP).  No -ffast-math: IEEE RN."""
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+    srcs = [_SRC, _SHIM, os.path.join(_HERE, "dd_oracle.h")]
+    if force or not os.path.exists(_SO) or any(os.path.getmtime(_SO) < os.path.getmtime(f) for f in srcs):
         subprocess.check_call(["gcc", "-std=c11", "-O2", "-fopenmp", "-fPIC", "-shared",
-                               "-o", _SO, _SRC, "-lm"])
+                               "-o", _SO, _SRC, _SHIM, "-lm"])
     return _SO
 
 
@@ -31,7 +33,8 @@ class _Opt(C.Structure):
     _fields_ = [("err_tol", C.c_double), ("trunc_tau", C.c_double),
                 ("max_inner_iter", C.c_int), ("n_threads", C.c_int),
                 ("schedule", C.c_int), ("eps_start", C.c_double),
-                ("coarsest_side", C.c_int), ("no_truncate", C.c_int), ("empty_init", C.c_int)]
+                ("coarsest_side", C.c_int), ("no_truncate", C.c_int), ("empty_init", C.c_int),
+                ("check_every", C.c_int)]
 
 
 class _Stats(C.Structure):
@@ -113,12 +116,12 @@ class Oracle:
 
     def __init__(self, mu, nu, eps, cell_size, *, err_tol=1e-6, trunc_tau=1e-15,
                  max_inner_iter=10000, n_threads=0, schedule=SCHED_FIXED, eps_start=0.0,
-                 coarsest_side=8, no_truncate=False, empty_init=False):
+                 coarsest_side=8, no_truncate=False, empty_init=False, check_every=1):
         self.mu = np.ascontiguousarray(mu, dtype=np.float64)
         self.nu = np.ascontiguousarray(nu, dtype=np.float64)
         n = self.mu.shape[0]
         opt = _Opt(err_tol, trunc_tau, max_inner_iter, n_threads, schedule, eps_start,
-                   coarsest_side, 1 if no_truncate else 0, 1 if empty_init else 0)
+                   coarsest_side, 1 if no_truncate else 0, 1 if empty_init else 0, check_every)
         self._h = C.c_void_p()
         rc = lib().ddo_init(C.byref(self._h), n, _dp(self.mu), _dp(self.nu), eps, cell_size,
                             C.byref(opt))

@@ -24,9 +24,8 @@ struct EvalParams {
     const double* mu;
     const double* logmu;
     const double* nu;
-    double* scratch;            // per cell: nu_cell[max_ny], g[max_ny], f[max_nx]
-    long long scratch_per_cell;
-    int max_ny;
+    double* scratch;            // per cell: nu_cell[ny], g[ny], f[nx] at scratch_off[cell]
+    const long long* scratch_off;
     double* cell_res;           // 3 per cell
     int coo;
     const long long* coo_off;

@@ -53,6 +53,7 @@ struct SweepParams {
     double tau;           // truncation threshold
     double err_tol;       // Err
     int max_iter;
+    int check_every;     // stop test cadence (A5): tested when it % check_every == 0
     int bcap;             // max Y-box side this launch handles
     int mode;             // 0: one CTA per cell; 1: work list in SMEM; 2: work list in global scratch
     unsigned char* gscratch;    // mode 2: per-CTA slice of global memory replacing SMEM

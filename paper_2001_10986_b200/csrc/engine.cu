@@ -98,6 +98,7 @@ struct dd_ctx {
     std::vector<SweepEvents> pending;
     std::vector<SweepEvents> free_events;
     double ms_last = 0, solve_ms_last = 0, ms_tot = 0, solve_ms_tot = 0;
+    long long failed_seen = 0;      // failed cells already reported by dd_synchronize
     long long launches_last = 0, launches_tot = 0, launches_pending = 0;
     std::string err;
 };
@@ -190,6 +191,14 @@ int harvest(dd_ctx* c) {
     return DD_OK;
 }
 
+int check_overflow(dd_ctx* c);
+// Wait for the context's work and report pool / box-size overflows.
+int sync_state(dd_ctx* c) {
+    int rc = harvest(c);
+    if (rc) return rc;
+    return check_overflow(c);
+}
+
 int check_overflow(dd_ctx* c) {
     int ov = 0;
     CK(cudaMemcpyAsync(&ov, c->counters + 6, sizeof(int), cudaMemcpyDeviceToHost, c->st));
@@ -271,6 +280,7 @@ int sweep(dd_ctx* c) {
     p.tau = c->tau;
     p.err_tol = c->opt.err_tol;
     p.max_iter = c->opt.max_inner_iter;
+    p.check_every = c->opt.check_every;
     p.box = c->box; p.off = c->off;
     p.pool_in = c->pool; p.scratch = c->scratch; p.bump = c->bump; p.cap = c->cap - c->halo_cap;
     p.alpha = part == 1 ? c->alphaA : c->alphaB;
@@ -344,7 +354,10 @@ int sweep(dd_ctx* c) {
 int product_init(dd_ctx* c) {
     Layer& Lr = c->L[c->cur];
     const long long need = (long long)Lr.nb * Lr.nb * Lr.side * Lr.side;
-    if (need > c->cap) { set_err(c, "pool capacity too small for the product initialisation"); return DD_ENOMEM; }
+    if (need > c->cap - c->halo_cap) {
+        set_err(c, "pool capacity too small for the product initialisation");
+        return DD_ENOMEM;
+    }
     CK(launch_product_init(c->box, c->off, c->pool, Lr.mass, Lr.nu, Lr.side, Lr.nb, c->st));
     const size_t n2 = (size_t)c->L[c->n_layers - 1].side * c->L[c->n_layers - 1].side;
     CK(cudaMemsetAsync(c->alphaA, 0, n2 * sizeof(double), c->st));
@@ -383,12 +396,12 @@ int evaluate(dd_ctx* c, double* out3, bool coo, long long* coo_count, int* cx, i
     std::vector<int4> hbox(nb2);
     CK(cudaMemcpyAsync(hbox.data(), c->box, nb2 * sizeof(int4), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
-    // per-cell union boxes on the host (sizes only) for scratch / COO layout
-    std::vector<long long> coo_off(ncells + 1, 0);
-    int max_ny = 1;
+    // per-cell union boxes on the host (sizes only) for the scratch and COO
+    // layouts: cell k's scratch (nu_cell, g: ny each; f: nx) starts at the
+    // prefix sum of the earlier cells' 2 ny + nx (no per-cell worst case)
+    std::vector<long long> coo_off(ncells + 1, 0), scr_off(ncells + 1, 0);
     int cr0, cr1;
     cell_rows(c, part, Lr.nb, &cr0, &cr1);
-    const int nx_max = 4 * Lr.s * Lr.s;
     for (int cell = 0; cell < ncells; ++cell) {
         const int cp = cell / nca, cq = cell % nca;
         int rlo, rhi, clo, chi;
@@ -406,20 +419,22 @@ int evaluate(dd_ctx* c, double* out3, bool coo, long long* coo_count, int* cx, i
                 y0 = std::min(y0, b.x); x0 = std::min(x0, b.y);
                 y1 = std::max(y1, b.x + b.z - 1); x1 = std::max(x1, b.y + b.w - 1);
             }
-        const int ny = y1 >= 0 ? (y1 - y0 + 1) * (x1 - x0 + 1) : 0;
-        max_ny = std::max(max_ny, ny);
-        const int nx = (rhi - rlo + 1) * (chi - clo + 1) * Lr.s * Lr.s;
+        const long long ny = y1 >= 0 ? (long long)(y1 - y0 + 1) * (x1 - x0 + 1) : 0;
+        const long long nx = (long long)(rhi - rlo + 1) * (chi - clo + 1) * Lr.s * Lr.s;
         const bool own = cp >= cr0 && cp < cr1;
-        coo_off[cell + 1] = coo_off[cell] + (own ? (long long)nx * ny : 0LL);
+        coo_off[cell + 1] = coo_off[cell] + (own ? nx * ny : 0LL);
+        scr_off[cell + 1] = scr_off[cell] + (own ? 2 * ny + nx : 0LL);
     }
-    const long long per_cell = 2LL * max_ny + nx_max;
-    const size_t need = (size_t)per_cell * ncells * sizeof(double);
+    const size_t need = (size_t)std::max(1LL, scr_off[ncells]) * sizeof(double) + (size_t)(ncells + 1) * sizeof(long long);
     if (need > c->eval_scratch_bytes) {
         if (c->eval_scratch) cudaFree(c->eval_scratch);
         c->eval_scratch = nullptr;
+        c->eval_scratch_bytes = 0;
         CK(cudaMalloc(&c->eval_scratch, need));
         c->eval_scratch_bytes = need;
     }
+    long long* d_scr_off = reinterpret_cast<long long*>(c->eval_scratch + std::max(1LL, scr_off[ncells]));
+    CK(cudaMemcpyAsync(d_scr_off, scr_off.data(), (ncells + 1) * sizeof(long long), cudaMemcpyHostToDevice, c->st));
     if ((size_t)3 * ncells > c->eval_res_n) {
         if (c->eval_res) cudaFree(c->eval_res);
         c->eval_res = nullptr;
@@ -432,7 +447,7 @@ int evaluate(dd_ctx* c, double* out3, bool coo, long long* coo_count, int* cx, i
     p.box = c->box; p.off = c->off; p.pool = c->pool;
     p.alpha = part == 1 ? c->alphaA : c->alphaB;
     p.mu = Lr.mu; p.logmu = Lr.logmu; p.nu = Lr.nu;
-    p.scratch = c->eval_scratch; p.scratch_per_cell = per_cell; p.max_ny = max_ny;
+    p.scratch = c->eval_scratch; p.scratch_off = d_scr_off;
     p.cell_res = c->eval_res;
     p.cr0 = cr0; p.cr1 = cr1;
     long long* d_coo_off = nullptr;
@@ -499,6 +514,7 @@ int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, d
     if (opt) c->opt = *opt;
     if (c->opt.err_tol <= 0) c->opt.err_tol = 1e-6;
     if (c->opt.max_inner_iter <= 0) c->opt.max_inner_iter = 10000;
+    if (c->opt.check_every <= 0) c->opt.check_every = 1;
     c->tau = c->opt.trunc_tau == 0.0 ? 1e-15 : (c->opt.trunc_tau < 0 ? 0.0 : c->opt.trunc_tau);
     if (c->opt.no_truncate) c->tau = 0.0;
     if (cost != DD_COST_SQEUCLID) { set_err(c, "only DD_COST_SQEUCLID is supported"); return DD_EINVAL; }
@@ -691,6 +707,7 @@ int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, d
 
 int dd_reset(dd_ctx* c) {
     if (!c) return DD_EINVAL;
+    CK(cudaSetDevice(c->device));
     c->cur = 0;
     c->stripe_lo = c->stripe_hi = 0;
     c->eps = (c->opt.schedule == DD_SCHED_LADDER) ? 2.0 / ((double)c->L[0].side * c->L[0].side) : c->eps_final;
@@ -705,6 +722,7 @@ int dd_set_eps(dd_ctx* c, double eps) {
 
 int dd_iterate(dd_ctx* c, int k) {
     if (!c || k < 0) return DD_EINVAL;
+    CK(cudaSetDevice(c->device));
     for (int i = 0; i < k; ++i) {
         int rc = sweep(c);
         if (rc) return rc;
@@ -714,11 +732,13 @@ int dd_iterate(dd_ctx* c, int k) {
 
 int dd_refine(dd_ctx* c) {
     if (!c) return DD_EINVAL;
+    CK(cudaSetDevice(c->device));
     if (c->cur + 1 >= c->n_layers) { set_err(c, "already at the finest layer"); return DD_EINVAL; }
     Layer& Lc = c->L[c->cur];
     Layer& Lf = c->L[c->cur + 1];
     CK(launch_refine(c->box, c->off, c->pool, c->box2, c->off2, c->scratch, Lc.nu, Lf.nu, Lc.mass, Lf.mass,
-                     Lc.nb, Lf.nb, Lc.side, Lf.side, c->cap, c->counters + 2, c->d_total, c->d_total + 1, c->st));
+                     Lc.nb, Lf.nb, Lc.side, Lf.side, c->cap - c->halo_cap, c->counters + 6, c->d_total,
+                     c->d_total + 1, c->st));
     std::swap(c->box, c->box2);
     std::swap(c->off, c->off2);
     std::swap(c->pool, c->scratch);
@@ -743,6 +763,7 @@ int dd_refine(dd_ctx* c) {
 
 int dd_run_schedule(dd_ctx* c) {
     if (!c) return DD_EINVAL;
+    CK(cudaSetDevice(c->device));
     if (c->opt.schedule != DD_SCHED_LADDER) { set_err(c, "dd_run_schedule needs DD_SCHED_LADDER"); return DD_EINVAL; }
     const int nf = c->L[c->n_layers - 1].side;
     const double kf = c->eps_final * (double)nf * nf;
@@ -759,19 +780,32 @@ int dd_run_schedule(dd_ctx* c) {
         int rc = dd_iterate(c, sweeps[k]);
         if (rc) return rc;
     }
-    return DD_OK;
+    // one wait at the end of the schedule: DD_ENOCONV if any cell hit max_inner_iter
+    return dd_synchronize(c);
 }
 
 int dd_synchronize(dd_ctx* c) {
     if (!c) return DD_EINVAL;
-    int rc = harvest(c);
+    CK(cudaSetDevice(c->device));
+    int rc = sync_state(c);
     if (rc) return rc;
-    return check_overflow(c);
+    // A6: cells that hit max_inner_iter since the last report (the sweeps
+    // themselves never wait on the host)
+    DevStats d;
+    CK(cudaMemcpy(&d, c->d_tot, sizeof(DevStats), cudaMemcpyDeviceToHost));
+    if (d.failed > c->failed_seen) {
+        set_err(c, "%lld cells did not converge within max_inner_iter = %d (state stays Y-feasible)",
+                (long long)d.failed - c->failed_seen, c->opt.max_inner_iter);
+        c->failed_seen = d.failed;
+        return DD_ENOCONV;
+    }
+    return DD_OK;
 }
 
 int dd_get_stats(dd_ctx* c, dd_sweep_stats* s) {
     if (!c || !s) return DD_EINVAL;
-    int rc = dd_synchronize(c);
+    CK(cudaSetDevice(c->device));
+    int rc = sync_state(c);
     if (rc) return rc;
     DevStats d;
     CK(cudaMemcpy(&d, c->d_last, sizeof(DevStats), cudaMemcpyDeviceToHost));
@@ -779,7 +813,7 @@ int dd_get_stats(dd_ctx* c, dd_sweep_stats* s) {
     fill_stats(d, s);
     s->ms = c->ms_last;
     s->solve_ms = c->solve_ms_last;
-    s->launches = 7;
+    s->launches = 8;
     if (d.failed) {
         set_err(c, "%d cells did not converge within max_inner_iter", d.failed);
         return DD_ENOCONV;
@@ -789,7 +823,8 @@ int dd_get_stats(dd_ctx* c, dd_sweep_stats* s) {
 
 int dd_get_totals(dd_ctx* c, dd_sweep_stats* s) {
     if (!c || !s) return DD_EINVAL;
-    int rc = dd_synchronize(c);
+    CK(cudaSetDevice(c->device));
+    int rc = sync_state(c);
     if (rc) return rc;
     DevStats d;
     CK(cudaMemcpy(&d, c->d_tot, sizeof(DevStats), cudaMemcpyDeviceToHost));
@@ -803,6 +838,7 @@ int dd_get_totals(dd_ctx* c, dd_sweep_stats* s) {
 
 int dd_set_stripe(dd_ctx* c, int row_lo, int row_hi) {
     if (!c) return DD_EINVAL;
+    CK(cudaSetDevice(c->device));
     const Layer& Lr = c->L[c->cur];
     if (row_lo == 0 && row_hi == 0) { c->stripe_lo = c->stripe_hi = 0; return DD_OK; }
     if (row_lo < 0 || row_hi > Lr.nb || row_lo >= row_hi || (row_lo & 1) || (row_hi & 1)) {
@@ -820,6 +856,7 @@ int dd_set_stripe(dd_ctx* c, int row_lo, int row_hi) {
 
 int dd_clear_rows(dd_ctx* c, int row, int nrows) {
     if (!c) return DD_EINVAL;
+    CK(cudaSetDevice(c->device));
     const Layer& Lr = c->L[c->cur];
     if (row < 0 || nrows < 0 || row + nrows > Lr.nb) { set_err(c, "rows out of range"); return DD_EINVAL; }
     if (nrows) CK(cudaMemsetAsync(c->box + (size_t)row * Lr.nb, 0, (size_t)nrows * Lr.nb * sizeof(int4), c->st));
@@ -840,9 +877,10 @@ long long pad2(long long a) { return (a + 1) & ~1LL; }
 
 int dd_export_rows(dd_ctx* c, int row, int nrows, void* buf, size_t* bytes) {
     if (!c || !bytes) return DD_EINVAL;
+    CK(cudaSetDevice(c->device));
     const Layer& Lr = c->L[c->cur];
     if (row < 0 || nrows <= 0 || row + nrows > Lr.nb) { set_err(c, "rows out of range"); return DD_EINVAL; }
-    int rc = dd_synchronize(c);
+    int rc = sync_state(c);
     if (rc) return rc;
     const int n = nrows * Lr.nb;
     std::vector<int4> hb(n);
@@ -869,9 +907,10 @@ int dd_export_rows(dd_ctx* c, int row, int nrows, void* buf, size_t* bytes) {
 
 int dd_import_rows(dd_ctx* c, int row, int nrows, const void* buf, size_t bytes) {
     if (!c || !buf) return DD_EINVAL;
+    CK(cudaSetDevice(c->device));
     const Layer& Lr = c->L[c->cur];
     if (row < 0 || nrows <= 0 || row + nrows > Lr.nb) { set_err(c, "rows out of range"); return DD_EINVAL; }
-    int rc = dd_synchronize(c);
+    int rc = sync_state(c);
     if (rc) return rc;
     const int n = nrows * Lr.nb;
     const char* b = (const char*)buf;
@@ -912,6 +951,7 @@ int dd_import_rows(dd_ctx* c, int row, int nrows, const void* buf, size_t bytes)
 
 int dd_copy_alpha(dd_ctx* c, int partition, int row0, int nrows, void* buf, int to_ctx) {
     if (!c || !buf || (partition != 1 && partition != 2)) return DD_EINVAL;
+    CK(cudaSetDevice(c->device));
     const Layer& Lr = c->L[c->cur];
     if (row0 < 0 || nrows < 0 || row0 + nrows > Lr.side) { set_err(c, "alpha rows out of range"); return DD_EINVAL; }
     double* a = (partition == 1 ? c->alphaA : c->alphaB) + (size_t)row0 * Lr.side;
@@ -924,6 +964,7 @@ int dd_copy_alpha(dd_ctx* c, int partition, int row0, int nrows, void* buf, int 
 
 int dd_y_accumulate(dd_ctx* c, unsigned long long* acc) {
     if (!c || !acc) return DD_EINVAL;
+    CK(cudaSetDevice(c->device));
     const Layer& Lr = c->L[c->cur];
     CK(launch_scatter_y(c->box, c->off, c->pool, Lr.nb, acc, Lr.side, c->st));
     CK(cudaStreamSynchronize(c->st));
@@ -932,6 +973,7 @@ int dd_y_accumulate(dd_ctx* c, unsigned long long* acc) {
 
 int dd_y_l1(dd_ctx* c, const unsigned long long* acc, double* l1_y) {
     if (!c || !acc || !l1_y) return DD_EINVAL;
+    CK(cudaSetDevice(c->device));
     const Layer& Lr = c->L[c->cur];
     CK(launch_l1y(acc, Lr.nu, Lr.side, c->partial, c->d_sums + 3, c->st));
     CK(cudaMemcpyAsync(l1_y, c->d_sums + 3, sizeof(double), cudaMemcpyDeviceToHost, c->st));
@@ -941,6 +983,7 @@ int dd_y_l1(dd_ctx* c, const unsigned long long* acc, double* l1_y) {
 
 int dd_phase_profile(dd_ctx* c, unsigned long long* out32) {
     if (!c || !out32) return DD_EINVAL;
+    CK(cudaSetDevice(c->device));
     int rc = harvest(c);
     if (rc) return rc;
     CK(k1_phase_read(out32));
@@ -949,6 +992,7 @@ int dd_phase_profile(dd_ctx* c, unsigned long long* out32) {
 
 int dd_get_cell_stats(dd_ctx* c, int* iters, int* box_side, double* mufu_ops, int* kcycles, int max_cells) {
     if (!c || max_cells < 0) return -DD_EINVAL;
+    if (cudaSetDevice(c->device) != cudaSuccess) return -DD_ECUDA;
     int rc = harvest(c);
     if (rc) return -rc;
     const Layer& Lr = c->L[c->cur];
@@ -974,18 +1018,21 @@ int dd_get_cell_stats(dd_ctx* c, int* iters, int* box_side, double* mufu_ops, in
 
 int dd_reset_totals(dd_ctx* c) {
     if (!c) return DD_EINVAL;
+    CK(cudaSetDevice(c->device));
     int rc = harvest(c);
     if (rc) return rc;
     CK(cudaMemsetAsync(c->d_tot, 0, sizeof(DevStats), c->st));
     CK(cudaStreamSynchronize(c->st));
     c->ms_tot = c->solve_ms_tot = 0;
     c->launches_tot = 0;
+    c->failed_seen = 0;
     return DD_OK;
 }
 
 int dd_primal_cost(dd_ctx* c, double* transport_cost, double* entropic) {
     if (!c) return DD_EINVAL;
-    int rc = dd_synchronize(c);
+    CK(cudaSetDevice(c->device));
+    int rc = sync_state(c);
     if (rc) return rc;
     double s[3];
     rc = evaluate(c, s, false, nullptr, nullptr, nullptr, nullptr);
@@ -997,7 +1044,8 @@ int dd_primal_cost(dd_ctx* c, double* transport_cost, double* entropic) {
 
 int dd_dual_gap(dd_ctx* c, double* primal, double* dual, double* rel_gap) {
     if (!c) return DD_EINVAL;
-    int rc = dd_synchronize(c);
+    CK(cudaSetDevice(c->device));
+    int rc = sync_state(c);
     if (rc) return rc;
     if (c->stripe_hi > c->stripe_lo) { set_err(c, "dd_dual_gap needs the whole layer (no stripe)"); return DD_EINVAL; }
     double s3[3];
@@ -1040,7 +1088,8 @@ int dd_dual_gap(dd_ctx* c, double* primal, double* dual, double* rel_gap) {
 
 int dd_marginal_error(dd_ctx* c, double* l1_x, double* l1_y) {
     if (!c) return DD_EINVAL;
-    int rc = dd_synchronize(c);
+    CK(cudaSetDevice(c->device));
+    int rc = sync_state(c);
     if (rc) return rc;
     double s[3];
     rc = evaluate(c, s, false, nullptr, nullptr, nullptr, nullptr);
@@ -1057,7 +1106,8 @@ int dd_marginal_error(dd_ctx* c, double* l1_x, double* l1_y) {
 
 int dd_get_state_info(dd_ctx* c, dd_state_info* info) {
     if (!c || !info) return DD_EINVAL;
-    int rc = dd_synchronize(c);
+    CK(cudaSetDevice(c->device));
+    int rc = sync_state(c);
     if (rc) return rc;
     Layer& Lr = c->L[c->cur];
     info->side = Lr.side;
@@ -1076,7 +1126,8 @@ int dd_get_state_info(dd_ctx* c, dd_state_info* info) {
 
 int dd_get_state(dd_ctx* c, int* boxes, long long* offsets, double* values, double* alpha_A, double* alpha_B) {
     if (!c) return DD_EINVAL;
-    int rc = dd_synchronize(c);
+    CK(cudaSetDevice(c->device));
+    int rc = sync_state(c);
     if (rc) return rc;
     Layer& Lr = c->L[c->cur];
     const int nb2 = Lr.nb * Lr.nb;
@@ -1102,6 +1153,7 @@ int dd_set_state(dd_ctx* c, int side, long long half_index, int last_partition, 
                  const long long* offsets, const double* values, long long n_values, const double* alpha_A,
                  const double* alpha_B) {
     if (!c || !boxes || !offsets || !values) return DD_EINVAL;
+    CK(cudaSetDevice(c->device));
     int k = 0;
     while (k < c->n_layers && c->L[k].side != side) ++k;
     if (k == c->n_layers) { set_err(c, "no layer of side %d", side); return DD_EINVAL; }
@@ -1124,7 +1176,7 @@ int dd_set_state(dd_ctx* c, int side, long long half_index, int last_partition, 
         ho[i] = o;
         o += (a + 1) & ~1LL;
     }
-    if (o > c->cap) { set_err(c, "state larger than the pool capacity"); return DD_ENOMEM; }
+    if (o > c->cap - c->halo_cap) { set_err(c, "state larger than the pool capacity"); return DD_ENOMEM; }
     std::vector<double> pool(std::max(1LL, o), 0.0);
     for (int i = 0; i < nb2; ++i) {
         const long long a = (long long)hb[i].z * hb[i].w;
@@ -1146,7 +1198,8 @@ int dd_set_state(dd_ctx* c, int side, long long half_index, int last_partition, 
 
 int dd_fetch_plan(dd_ctx* c, int format, void* buf, size_t* bytes) {
     if (!c || !bytes) return DD_EINVAL;
-    int rc = dd_synchronize(c);
+    CK(cudaSetDevice(c->device));
+    int rc = sync_state(c);
     if (rc) return rc;
     Layer& Lr = c->L[c->cur];
     if (format == DD_PLAN_BASIC_MARGINALS) {
@@ -1220,6 +1273,7 @@ int dd_measure_mufu_peak(int device, double* ops_per_s) {
 
 void dd_free(dd_ctx* c) {
     if (!c) return;
+    cudaSetDevice(c->device);
     if (c->st) cudaStreamSynchronize(c->st);
     free_all(c);
     delete c;

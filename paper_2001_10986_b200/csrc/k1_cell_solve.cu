@@ -1253,7 +1253,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         PROF_ADD(0, tb - ta); PROF_ADD(1, tc - tb); PROF_ADD(2, td - tc); PROF_ADD(3, te - td);
         PROF_ADD(4, tf - te); PROF_ADD(5, tg - tf);
         ++it;
-        if (err <= tol) break;
+        if (err <= tol && it % p.check_every == 0) break;
         if (it >= p.max_iter || !(err == err)) { co.flags |= 1; break; }
         float2* t = Fc; Fc = Fn; Fn = t;
     }
@@ -1552,14 +1552,18 @@ cudaError_t launch_k0(const SweepParams& p, int b0, int b1, int* lists, int* cou
 
 template <int NT, bool BIG, int MINB>
 static cudaError_t launch_tier(const SweepParams& p, int grid, size_t smem, cudaStream_t st) {
-    static size_t attr = 0;
+    // the SMEM opt-in is a per-device function attribute: cache it per device
+    static size_t attr[64] = {0};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
     // opt in whenever the request grows: the 48 KB default covers static +
     // dynamic SMEM together, so a dynamic size just under 48 KB can fail too
-    if (smem > attr) {
-        cudaError_t e = cudaFuncSetAttribute(k1_cell_solve<NT, BIG, MINB>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (smem > attr[dev]) {
+        e = cudaFuncSetAttribute(k1_cell_solve<NT, BIG, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        attr = smem;
+        attr[dev] = smem;
     }
     k1_cell_solve<NT, BIG, MINB><<<grid, NT, smem, st>>>(p);
     return cudaGetLastError();

@@ -189,7 +189,7 @@ __global__ void k_refine_boxes(const int4* __restrict__ cbox, int4* __restrict__
 
 // nu_i^0(y) = nu(y) nuhat_{Pa(i)}(pa(y)) / nuhat(pa(y)) * mu(X_i) / muhat(Xhat_{Pa(i)}), 0/0 := 0.
 __global__ void k_refine_fill(const int4* __restrict__ cbox, const long long* __restrict__ coff,
-                              const double* __restrict__ cpool, const int4* __restrict__ fbox,
+                              const double* __restrict__ cpool, int4* __restrict__ fbox,
                               const long long* __restrict__ foff, double* __restrict__ fpool,
                               const double* __restrict__ cnu, const double* __restrict__ fnu,
                               const double* __restrict__ cmass, const double* __restrict__ fmass,
@@ -202,7 +202,12 @@ __global__ void k_refine_fill(const int4* __restrict__ cbox, const long long* __
     const long long area = (long long)fb.z * fb.w;
     const long long o = foff[i];
     if (o + area > cap) {
-        if (threadIdx.x == 0) atomicOr(overflow, 1);
+        // pool overflow: flag it (dd_synchronize -> DD_ENOMEM) and leave an
+        // empty box so no later kernel reads past the pool
+        if (threadIdx.x == 0) {
+            atomicOr(overflow, 1);
+            fbox[i] = make_int4(fb.x, fb.y, 0, 0);
+        }
         return;
     }
     const double ratio = fmass[i] / cmass[j];
@@ -294,9 +299,9 @@ __global__ void k_eval_cells(EvalParams p) {
     }
     const int br = y1 >= 0 ? y1 - y0 + 1 : 0, bc = x1 >= 0 ? x1 - x0 + 1 : 0;
     const int nx = ar * ac, ny = br * bc;
-    double* nuc = p.scratch + (long long)cell * p.scratch_per_cell;
-    double* g = nuc + p.max_ny;
-    double* f = g + p.max_ny;
+    double* nuc = p.scratch + p.scratch_off[cell];      // [ny] | g [ny] | f [nx]
+    double* g = nuc + ny;
+    double* f = g + ny;
     const double h = 1.0 / p.side;
     const double eps = p.eps;
     for (int y = tid; y < ny; y += blockDim.x) {

@@ -29,6 +29,10 @@ EXPORTS = ["dd_init", "dd_iterate", "dd_set_eps", "dd_refine", "dd_run_schedule"
            "dd_last_error", "dd_version"]
 
 
+class NotConverged(RuntimeError):
+    """DD_ENOCONV: some cell hit max_inner_iter (reading A6); the state stays Y-feasible."""
+
+
 class Options(C.Structure):
     _fields_ = [("err_tol", C.c_double), ("trunc_tau", C.c_double),
                 ("max_inner_iter", C.c_int), ("check_every", C.c_int), ("n_gpus", C.c_int),
@@ -124,11 +128,12 @@ class DD:
     def __init__(self, mu, nu, eps, cell_size, *, err_tol=1e-6, trunc_tau=1e-15,
                  max_inner_iter=10000, schedule=SCHED_FIXED, eps_start=0.0, coarsest_side=8,
                  no_truncate=False, device=0, pool_capacity=0, stream=None, device_input=False,
-                 bcap_main=0, bcap_big=0, cold_refine=False):
+                 bcap_main=0, bcap_big=0, cold_refine=False, check_every=1):
         opt = Options()
         opt.err_tol = err_tol
         opt.trunc_tau = trunc_tau
         opt.max_inner_iter = max_inner_iter
+        opt.check_every = check_every
         opt.schedule = schedule
         opt.eps_start = eps_start
         opt.coarsest_side = coarsest_side
@@ -175,6 +180,8 @@ class DD:
 
     def _check(self, rc, what, allow=(OK,)):
         if rc not in allow:
+            if rc == ENOCONV:
+                raise NotConverged(f"{what}: {self.last_error()}")
             raise RuntimeError(f"{what} failed rc={rc}: {self.last_error()}")
         return rc
 

@@ -284,3 +284,44 @@ def test_ladder_s8_big_tiers_128(DD):
     assert abs(cg - co) <= 1e-5 * co, (cg, co)
     lx, ly = g.marginal_error()
     assert lx <= 1e-6 and ly <= 1e-6
+
+
+@pytest.mark.parametrize("dm,ds", [(5e-6, 0.0), (0.0, 1e-3), (2e-6, 1e-4)])
+def test_l1y_known_deviation_gpu_vs_oracle(DD, dm, ds):
+    """A state of known Y-deviation (tests/test_oracle_pins.py): GPU l1_y =
+    oracle l1_y = the closed form, after the same import."""
+    from test_oracle_pins import _perturbed_product_state
+    mu, nu, st, dev = _perturbed_product_state(dm, ds)
+    want = np.abs(dev).sum()
+    g = DD(mu, nu, 2.0 / 32**2, 4)
+    g.set_state(st)
+    o = Oracle(mu, nu, 2.0 / 32**2, 4, empty_init=True)
+    o.set_state(st)
+    _, lyg = g.marginal_error()
+    _, lyo = o.marginal_error()
+    assert abs(lyg - want) <= 1e-13 + 1e-9 * want, (lyg, want)
+    assert abs(lyg - lyo) <= 1e-13 + 1e-9 * want
+
+
+def test_l1y_after_ladder_gpu_vs_oracle(DD):
+    """l1_y of the GPU's own state vs the oracle's evaluation of the same state."""
+    mu, nu = config_images(2)
+    g = DD(mu, nu, 0.5 / 64**2, 4, schedule=1, coarsest_side=16, eps_start=1.0)
+    g.run_schedule()
+    st = g.get_state()
+    o = Oracle(mu, nu, 0.5 / 64**2, 4, empty_init=True)
+    o.set_state(st)
+    lxg, lyg = g.marginal_error()
+    lxo, lyo = o.marginal_error()
+    assert abs(lyg - lyo) <= 1e-15 + 1e-9 * lyo, (lyg, lyo)
+    assert abs(lxg - lxo) <= 1e-9 + 1e-6 * lxo, (lxg, lxo)
+    assert lyg <= 1e-6 and lxg <= 1e-6
+
+
+def test_pool_overflow_reports_enomem(DD):
+    """A pool too small for the refined state: the refinement flags it
+    (no out-of-bounds reads), dd_synchronize returns DD_ENOMEM."""
+    mu, nu = config_images(2)
+    g = DD(mu, nu, 0.5 / 64**2, 4, schedule=1, coarsest_side=16, pool_capacity=16 * 16 * 16 * 16 + 64)
+    with pytest.raises(RuntimeError, match="rc=6"):
+        g.run_schedule()

@@ -411,3 +411,45 @@ def test_pd_gap_weak_duality_and_convergence():
     assert all(g > -1e-9 for g in gaps)
     assert all(b < a for a, b in zip(gaps, gaps[1:]))
     assert gaps[-1] < 1e-7
+
+
+def _perturbed_product_state(delta_move, delta_scale):
+    """The product coupling nu_i = ||mu_i|| nu at 32^2 (Y-feasible: sum_i nu_i
+    = nu), then (a) mass delta_move moved inside basic cell 5's box
+    from its largest entry to one 13 rows / 5 columns away, (b) every nu_i
+    scaled by (1 + delta_scale).  nu is not symmetric, so a transposed or
+    shifted accumulation fails by far more than the deviation."""
+    mu, nu = config_images(1)
+    o = Oracle(mu, nu, 2.0 / 32**2, 4)
+    st = o.get_state()
+    v = st["values"].copy()
+    y0, x0, hr, hc = st["boxes"][5]
+    assert (y0, x0, hr, hc) == (0, 0, 32, 32)
+    o5 = st["offsets"][5]
+    src = int(np.argmax(v[o5:o5 + 1024]))
+    r, c = divmod(src, 32)
+    dst = ((r + 13) % 32) * 32 + (c + 5) % 32
+    assert v[o5 + src] > 2 * delta_move
+    v[o5 + src] -= delta_move
+    v[o5 + dst] += delta_move
+    v *= 1.0 + delta_scale
+    st["values"] = v
+    dev = delta_scale * nu.ravel().copy()          # the known deviation sum_i nu_i - nu
+    dev[src] -= delta_move * (1.0 + delta_scale)
+    dev[dst] += delta_move * (1.0 + delta_scale)
+    return mu, nu, st, dev
+
+
+@pytest.mark.parametrize("dm,ds", [(5e-6, 0.0), (0.0, 1e-3), (1e-6, 0.0), (2e-6, 1e-4)])
+def test_marginal_error_l1y_pin(dm, ds):
+    """Reading A18: l1_y = sum_y |sum_i nu_i(y) - nu(y)|.  A state of known
+    deviation: moving mass d inside one box gives exactly 2 d; scaling every
+    nu_i by (1 + e) gives e ||nu|| = e.  Pins ddo_marginal_error's l1_y."""
+    mu, nu, st, dev = _perturbed_product_state(dm, ds)
+    o = Oracle(mu, nu, 2.0 / 32**2, 4, empty_init=True)
+    o.set_state(st)
+    _, ly = o.marginal_error()
+    want = np.abs(dev).sum()                       # 2 dm, resp. ds, when only one is set
+    if dm == 0.0 or ds == 0.0:
+        assert abs(want - (2 * dm + ds)) <= 1e-15
+    assert abs(ly - want) <= 1e-13 + 1e-10 * want, (ly, want)

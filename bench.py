@@ -38,10 +38,11 @@ UNIT = "cell_solves/s"
 def _args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--pairs", type=int, default=5, help="image pairs cycled through the timed steps (N=1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -175,6 +176,126 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------------- finest-sweep tools --
+def run_all_but_last(g, n, coarsest, kappa_final, eps_start):
+    """Reset g and run the bench's schedule up to (not including) its last
+    sweep, stage by stage; returns (schedule, per-sweep stats of the last
+    finest-layer stage before it)."""
+    from paper_2001_10986_b200 import build_schedule
+    g.reset()
+    sched = build_schedule(n, coarsest, kappa_final, eps_start)
+    total = sum(w for _, _, w in sched)
+    side, done = coarsest, 0
+    for sd, kappa, sweeps in sched:
+        while side < sd:
+            g.refine()
+            side *= 2
+        g.set_eps(kappa / sd**2)
+        k = sweeps if done + sweeps < total else sweeps - 1
+        g.iterate(k)
+        done += k
+    return sched
+
+
+def finest_sweep_rate(g, n, coarsest, kappa_final, eps_start, peak):
+    """SURVEY 8(d) metric 1(i): cell solves/s of the last (steady-state,
+    final-eps) sweeps of the finest layer, device time per sweep from the
+    library's CUDA events."""
+    run_all_but_last(g, n, coarsest, kappa_final, eps_start)
+    g.synchronize()
+    g.iterate(1)
+    st = g.stats()
+    return {"cells": st["cells"], "ms": st["ms"], "solve_ms": st["solve_ms"],
+            "value": st["cells"] / (st["ms"] * 1e-3), "unit": UNIT, "iters_per_cell": st["iters_sum"] / st["cells"],
+            "iters_max": st["iters_max"], "mufu_frac": st["mufu_ops"] / (st["solve_ms"] * 1e-3) / peak,
+            "sweep": f"last sweep of the schedule (partition B, {n}^2, kappa={kappa_final})"}
+
+
+def cpu_baseline_finest(g, cfg, w, budget_s=20.0):
+    """The oracle as it stands on the host cores, timed on the workload's own
+    cells: the state before the last cfg sweep of the finest layer (the GPU
+    runs the schedule up to there, untimed; the oracle only imports it -- this
+    is a timing sample, not a parity input), then a box-side-stratified sample
+    of that sweep's composite cells solved by the dense fp64 oracle with one
+    OpenMP thread per cell (as its sweep does).  Bins the sample cannot afford
+    are extrapolated from the measured dense-term rate; a 1-thread run of the
+    small bins gives the per-core rate."""
+    from oracle import Oracle
+    n, s = w["n"], w["s"]
+    eps = w["kappa_final"] / n**2
+    run_all_but_last(g, n, w["coarsest"], w["kappa_final"], w["eps_start"])
+    before = g.get_state()
+    g.iterate(1)
+    it, box, _, _ = g.cell_stats()
+    part = g.state_info()["last_partition"]
+    mu, nu = g._keep_host
+    cores = os.cpu_count() or 1
+    try:
+        model = [ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo") if ln.startswith("model name")][0]
+    except Exception:
+        model = "unknown"
+    nx = np.full(it.size, 4 * s * s, np.float64)      # |X_J| (interior cells; edges/corners smaller)
+    terms = it.astype(np.float64) * nx * 2.0 * box.astype(np.float64) ** 2   # dense exps of each solve
+    bins = [(0, 24), (24, 40), (40, 56), (56, 90), (90, 120), (120, 250), (250, 10**6)]
+    rng = np.random.default_rng(cfg)
+    t_term = 4e-9                                      # prior s per dense term and core (refined below)
+
+    def measure(n_threads, max_bin, budget):
+        o = Oracle(mu, nu, eps, s, empty_init=True, n_threads=n_threads)
+        o.set_state(before)
+        out, used = [], set()
+        for lo, hi in bins[:max_bin]:
+            cand = np.nonzero((box > lo) & (box <= hi))[0]
+            if not cand.size:
+                continue
+            cand = rng.permutation(cand)
+            pick, est = [], 0.0
+            for c in cand:                           # up to 2 cells per thread within the bin's budget
+                if len(pick) >= 2 * n_threads or c in used:
+                    continue
+                e = terms[c] * t_term
+                if est + e > budget * n_threads / len(bins):
+                    continue
+                pick.append(int(c))
+                est += e
+            if not pick:
+                continue
+            used.update(pick)
+            t0 = time.perf_counter()
+            o.solve_cells(part, np.array(pick), concurrent=True)
+            dt = time.perf_counter() - t0
+            out.append(dict(bin=f"({lo},{hi}]", cells=len(pick), seconds=dt, cells_per_s=len(pick) / dt,
+                            terms_per_s=float(terms[pick].sum()) / dt, n_in_sweep=int(cand.size)))
+        return out
+
+    t_all = time.perf_counter()
+    mt = measure(cores, len(bins), budget_s)
+    st1 = measure(1, 3, budget_s / 3)
+    term_rate = sum(b["terms_per_s"] * b["seconds"] for b in mt) / max(1e-9, sum(b["seconds"] for b in mt))
+    # extrapolated sweep time: measured bins by their cells/s, the rest by the term rate
+    sweep_s = 0.0
+    measured = {b["bin"]: b for b in mt}
+    for lo, hi in bins:
+        sel = (box > lo) & (box <= hi)
+        k = f"({lo},{hi}]"
+        if not sel.any():
+            continue
+        if k in measured:
+            sweep_s += sel.sum() / measured[k]["cells_per_s"]
+        else:
+            sweep_s += terms[sel].sum() / term_rate
+    rate1 = sum(b["cells"] for b in st1) / max(1e-9, sum(b["seconds"] for b in st1))
+    ncells = int(it.size)
+    return {"value": ncells / sweep_s, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"cfg{cfg} finest layer ({n}^2, s={s}, kappa={w['kappa_final']}): the last sweep's "
+                      f"{ncells} composite cells from the state before it; {sum(b['cells'] for b in mt)} cells "
+                      f"sampled by union-box side (dense fp64 oracle, OpenMP {cores} threads, one per cell), "
+                      f"unsampled bins extrapolated from the measured dense-term rate",
+            "cpu_model": model, "extrapolated_sweep_s": sweep_s, "bins": mt,
+            "one_thread": {"bins": st1, "cells_per_s": rate1},
+            "dense_terms_per_s": term_rate, "seconds": time.perf_counter() - t_all}
+
+
 # ------------------------------------------------------------------ our leg --
 def main():
     args = _args()
@@ -201,14 +322,23 @@ def main():
     w = _workload(args.config)
     n, s = w["n"], w["s"]
     eps = w["kappa_final"] / n**2
-    mu_h, nu_h = config_images(args.config, pair=0)      # one problem, striped over the ranks
-    mu_d = torch.from_numpy(mu_h).to(dev)
-    nu_d = torch.from_numpy(nu_h).to(dev)
     stream = torch.cuda.Stream(dev)          # a real stream handle (the default stream is 0)
     torch.cuda.set_stream(stream)
     kw = dict(err_tol=w["err_tol"], trunc_tau=w["trunc_tau"], schedule=SCHED_LADDER,
               eps_start=w["eps_start"], coarsest_side=w["coarsest"], device=local)
-    g = DD(mu_d, nu_d, eps, s, device_input=True, stream=stream.cuda_stream, **kw)
+    # 5 image pairs (seeds 2k+1, 2k+2), all resident in HBM; the
+    # timed steps cycle through them.  Multi-GPU: one problem striped.
+    npairs = max(1, args.pairs) if world == 1 else 1
+    ctxs, host = [], []
+    for k in range(npairs):
+        mu_h, nu_h = config_images(args.config, pair=k)
+        mu_d = torch.from_numpy(mu_h).to(dev)
+        nu_d = torch.from_numpy(nu_h).to(dev)
+        c = DD(mu_d, nu_d, eps, s, device_input=True, stream=stream.cuda_stream, **kw)
+        c._keep_host = (mu_h, nu_h)
+        ctxs.append(c)
+        host.append((mu_h, nu_h))
+    g = ctxs[0]
     run = None
     if world > 1:
         from paper_2001_10986_b200.striped import StripedRun, TorchTransport
@@ -222,36 +352,42 @@ def main():
             striped.run_schedule(n, w["coarsest"], w["kappa_final"], w["eps_start"])
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    for _ in range(args.warmup):
-        g.reset()
-        solve(g, run)
-        g.synchronize()
-    # ---- timed region: K steps, per-step CUDA events on the library's stream
-    g.reset_totals()
+    for k in range(max(args.warmup, npairs if args.warmup > 0 else 0)):
+        c = ctxs[k % npairs]
+        c.reset()
+        solve(c, run)
+        c.synchronize()
+    # ---- timed region: K steps (pair k mod 5), per-step CUDA events on the library's stream
+    for c in ctxs:
+        c.reset_totals()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     clocks = ClockSampler(local)
     clocks.start()
-    step_ms = []
-    cells_step = []
-    for _ in range(args.steps):
+    step_ms, cells_step, step_pair = [], [], []
+    for k in range(args.steps):
+        c = ctxs[k % npairs]
         flush.fill_(1.0)                       # L2 flush between timed steps (256 MB > 126 MB L2)
-        g.reset()                              # state back to the product coupling (untimed)
+        c.reset()                              # state back to the product coupling (untimed)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         c0 = run.cells_solved if run else 0
         e0.record(stream)
-        solve(g, run)
+        solve(c, run)
         e1.record(stream)
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
+        step_pair.append(k % npairs)
         cells_step.append(run.cells_solved - c0 if run else None)
     torch.cuda.synchronize(dev)
     clk = clocks.stop()
     if world > 1:
         dist.barrier()
-    tot = g.totals()
+    tots = [c.totals() for c in ctxs]
+    tot = {key: sum(t[key] for t in tots) for key in ("cells", "iters_sum", "failed", "mufu_ops", "solve_ms",
+                                                       "launches", "big_cells")}
+    tot["max_box"] = max(t["max_box"] for t in tots)
     my_ms = float(np.sum(step_ms))
     if run is not None:
         all_cells = float(np.sum(cells_step))          # whole-problem solves (replicated layers once)
@@ -260,13 +396,33 @@ def main():
         wall_ms, all_cells = my_ms, float(tot["cells"])
     cells_per_step = all_cells / args.steps
     value = all_cells / (wall_ms * 1e-3)
-    # ---- quality of the final state (outside the timed region)
+    per_pair = None
+    if run is None and npairs > 1:
+        pair_rate = {}
+        for k in range(npairs):
+            ms = [m for m, q in zip(step_ms, step_pair) if q == k]
+            if ms:
+                pair_rate[k] = tots[k]["cells"] / (np.sum(ms) * 1e-3)
+        vals = list(pair_rate.values())
+        per_pair = {"cell_solves_per_s": {str(k): v for k, v in pair_rate.items()},
+                    "median": float(np.median(vals)), "min": float(np.min(vals)),
+                    "ms_per_solve": {str(k): float(np.mean([m for m, q in zip(step_ms, step_pair) if q == k]))
+                                     for k in pair_rate}}
+    # ---- quality of the final state of pair 0 (outside the timed region)
+    g.reset()
+    solve(g, run)
     if run is not None:
         cost, ent = run.primal_cost()
         l1x, l1y = run.marginal_error()
+        gap = None
     else:
+        g.synchronize()
         cost, ent = g.primal_cost()
         l1x, l1y = g.marginal_error()
+        t0 = time.perf_counter()
+        _, _, gap = g.dual_gap()
+        gap = {"rel_pd_gap": gap, "seconds": time.perf_counter() - t0,
+               "def": "eq. RelPDGap (P:1711-1717), glued dual candidate (Sec. 6.3)"}
     last = g.stats()
 
     # ---- roofline of the dominant kernel (K1): algorithmic MUFU ops / K1 time
@@ -286,10 +442,14 @@ def main():
                 "peak_nominal": nominal / 1e12, "traffic": prof_traffic, "traffic_unit": traffic_unit,
                 "kernel": "k1_cell_solve", "kernel_share_of_step": k1_ms / my_ms,
                 "mufu_ops_per_step": tot["mufu_ops"] / args.steps}
+    finest = None
+    if run is None:
+        finest = finest_sweep_rate(g, n, w["coarsest"], w["kappa_final"], w["eps_start"], peak)
 
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
+        mu_h, nu_h = host[0]
         mu_p = torch.from_numpy(mu_h).pin_memory()
         nu_p = torch.from_numpy(nu_h).pin_memory()
         e2e_ms = []
@@ -317,14 +477,15 @@ def main():
             if k > 0:
                 e2e_ms.append(dt * 1e3)
         e2e_ms_med = float(np.median(e2e_ms))
-        e2e = {"value": cells_per_step / (e2e_ms_med * 1e-3),
+        cells_pair0 = tots[0]["cells"] / max(1, sum(1 for q in step_pair if q == 0)) if run is None else cells_per_step
+        e2e = {"value": cells_pair0 / (e2e_ms_med * 1e-3),
                "unit": UNIT, "h2d_bytes_per_step": int(mu_h.nbytes + nu_h.nbytes),
                "d2h_bytes_per_step": 4 * 8, "ms_per_step": e2e_ms_med,
-               "path": "dd_init(host) + dd_run_schedule + dd_primal_cost + dd_marginal_error + dd_free"}
+               "path": "dd_init(host) + dd_run_schedule + dd_primal_cost + dd_marginal_error + dd_free (pair 0)"}
 
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_baseline(args.config)
+        cb = cpu_baseline_finest(g, args.config, w)
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": wall_ms / args.steps, "higher_is_better": True,
@@ -333,14 +494,15 @@ def main():
                             "balance and marginal sums",
             "data": "synthetic",
             "config": {**{k: w[k] for k in ("workload", "n", "s", "kappa_final", "err_tol", "trunc_tau")},
-                       "global_batch": 1,
+                       "image_pairs": npairs, "global_batch": 1,
                        "parallelism": f"stripes{world} (NCCL send/recv of boundary rows)" if world > 1 else "single",
                        "l2": "flushed between steps (256 MB write); nu_i pool > L2"},
             "time_to_solution_ms": wall_ms / args.steps,
             "cells_per_step": cells_per_step,
             "iters_per_cell": tot["iters_sum"] / max(1, tot["cells"]),
-            "final": {"transport_cost": cost, "entropic": ent, "l1_x": l1x, "l1_y": l1y,
-                      "entries_per_px": last["entries"] / n**2, "max_box": tot["max_box"],
+            "pairs": per_pair, "finest_sweep": finest,
+            "final": {"pair": 0, "transport_cost": cost, "entropic": ent, "l1_x": l1x, "l1_y": l1y,
+                      "pd_gap": gap, "entries_per_px": last["entries"] / n**2, "max_box": tot["max_box"],
                       "big_cells": tot["big_cells"], "failed": tot["failed"]},
             "roofline": roofline, "clocks": clk, "gpu_launches": int(tot["launches"]),
             "e2e": e2e, "cpu_baseline": cb}

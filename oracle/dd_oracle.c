@@ -621,6 +621,33 @@ int ddo_solve_cells(ddo_ctx* c, int part, int n, const int* cells, int* iters) {
     return rc;
 }
 
+/* The same for a batch of cells solved concurrently, one OpenMP thread per
+ * cell as in a sweep (cells of one partition are disjoint).  Used to
+ * time the oracle's sweep throughput on a sample of a sweep's cells. */
+int ddo_solve_cells_par(ddo_ctx* c, int part, int n, const int* cells, int* iters) {
+    if (!c || (part != 1 && part != 2) || n < 0 || (n && !cells)) return DDO_EINVAL;
+    int nc = n_cells(c, part);
+    for (int k = 0; k < n; ++k)
+        if (cells[k] < 0 || cells[k] >= nc) { set_err(c, "cell %d out of range", cells[k]); return DDO_EINVAL; }
+    cellres_t* res = (cellres_t*)calloc((size_t)(n > 0 ? n : 1), sizeof(cellres_t));
+    int* rcs = (int*)calloc((size_t)(n > 0 ? n : 1), sizeof(int));
+    if (!res || !rcs) { free(res); free(rcs); return DDO_ENOMEM; }
+#ifdef _OPENMP
+    int nt = c->opt.n_threads > 0 ? c->opt.n_threads : omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nt)
+#endif
+    for (int k = 0; k < n; ++k) rcs[k] = solve_cell(c, part, cells[k], &res[k]);
+    int rc = DDO_OK;
+    for (int k = 0; k < n; ++k) {
+        if (iters) iters[k] = res[k].iters;
+        if (rcs[k] == DDO_ENOMEM) rc = DDO_ENOMEM;
+        if (!rc && res[k].flag) rc = res[k].flag;
+    }
+    free(res);
+    free(rcs);
+    return rc;
+}
+
 int ddo_iterate(ddo_ctx* c, int n_half_iters) {
     if (!c) return DDO_EINVAL;
     int rc = DDO_OK;

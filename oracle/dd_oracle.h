@@ -90,6 +90,9 @@ int ddo_iterate(ddo_ctx* c, int n_half_iters);
  * as in Sec. 6.3: primal = KL(pi|K) - ||K||, dual = J(u_hat, v_hat) - ||K||. */
 int ddo_dual_gap(ddo_ctx* c, double* primal, double* dual, double* rel);
 int ddo_solve_cells(ddo_ctx* c, int part, int n, const int* cells, int* iters);
+/* The same with the listed cells solved concurrently (OpenMP over cells, as
+ * in a sweep); for timing the oracle on a sample of a sweep. */
+int ddo_solve_cells_par(ddo_ctx* c, int part, int n, const int* cells, int* iters);
 int ddo_refine(ddo_ctx* c);
 int ddo_run_schedule(ddo_ctx* c);
 int ddo_primal_cost(ddo_ctx* c, double* transport_cost, double* entropic);

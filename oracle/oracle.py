@@ -65,6 +65,7 @@ def lib():
         _lib.ddo_set_eps.argtypes = [p, d]
         _lib.ddo_iterate.argtypes = [p, i]
         _lib.ddo_solve_cells.argtypes = [p, i, i, p, p]
+        _lib.ddo_solve_cells_par.argtypes = [p, i, i, p, p]
         _lib.ddo_dual_gap.argtypes = [p, dp, dp, dp]
         _lib.ddo_refine.argtypes = [p]
         _lib.ddo_run_schedule.argtypes = [p]
@@ -156,11 +157,14 @@ class Oracle:
         self._check(lib().ddo_dual_gap(self._h, C.byref(a), C.byref(b), C.byref(r)), "dual_gap")
         return a.value, b.value, r.value
 
-    def solve_cells(self, part, cells):
-        """Algorithm 2 lines 8-13 for the listed cells of partition part only."""
+    def solve_cells(self, part, cells, concurrent=False):
+        """Algorithm 2 lines 8-13 for the listed cells of partition part only
+        (concurrent: one OpenMP thread per cell, as in a sweep; else one cell
+        at a time, each half-iteration's outputs spread over the threads)."""
         cells = np.ascontiguousarray(cells, np.int32)
         iters = np.zeros(max(cells.size, 1), np.int32)
-        self._check(lib().ddo_solve_cells(self._h, part, cells.size, cells.ctypes.data, iters.ctypes.data),
+        fn = lib().ddo_solve_cells_par if concurrent else lib().ddo_solve_cells
+        self._check(fn(self._h, part, cells.size, cells.ctypes.data, iters.ctypes.data),
                     "solve_cells", (OK, ENOCONV))
         return iters[:cells.size]
 

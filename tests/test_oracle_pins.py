@@ -375,13 +375,16 @@ def test_validation_errors(case):
         Oracle(mu, nu, 1.0, s)
 
 
-def test_solve_cells_equals_sweep_subset():
-    """ddo_solve_cells on every cell of a partition reproduces ddo_iterate."""
+@pytest.mark.parametrize("concurrent", [False, True])
+def test_solve_cells_equals_sweep_subset(concurrent):
+    """ddo_solve_cells (one cell at a time with the half-iterations threaded,
+    or the cells concurrently) on every cell of a partition reproduces
+    ddo_iterate bit for bit."""
     mu, nu = config_images(1)
     a = Oracle(mu, nu, 2 / 32**2, 4)
     b = Oracle(mu, nu, 2 / 32**2, 4)
     a.iterate(1)
-    b.solve_cells(1, np.arange(16))
+    b.solve_cells(1, np.arange(16), concurrent=concurrent)
     assert np.array_equal(a.basic_marginals_dense(), b.basic_marginals_dense())
 
 

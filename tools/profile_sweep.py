@@ -26,7 +26,8 @@ ap.add_argument("--quiet", action="store_true")
 ap.add_argument("--bcap", type=int, default=0)
 ap.add_argument("--bcap-big", type=int, default=0)
 ap.add_argument("--json", default="")
-ap.add_argument("--cells-npz", default="", help="dump per-cell (iters, box, mufu) of every sweep at side >= n/2")
+ap.add_argument("--cells-npz", default="", help="dump per-cell (iters, box, mufu, kcycles) of every sweep at side >= n/2")
+ap.add_argument("--cells-all", action="store_true", help="--cells-npz for every layer")
 a = ap.parse_args()
 p = CONFIGS[a.cfg]
 n, s = p["n"], p["s"]
@@ -54,7 +55,7 @@ for k, (side, kappa, sweeps) in enumerate(sched):
                    **{q: st[q] for q in ("cells", "iters_sum", "iters_max", "failed", "entries", "ms",
                                          "solve_ms", "big_cells", "max_box", "fallbacks", "mufu_ops")})
         rows.append(row)
-        if a.cells_npz and side >= n // 2:
+        if a.cells_npz and (side >= n // 2 or a.cells_all):
             it, bx, mf, kc = g.cell_stats()
             cell_dump[f"s{side}_k{kappa}_j{j}"] = np.stack([it, bx, mf.astype(np.float64), kc])
         if not a.quiet:

@@ -42,7 +42,11 @@ def _args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=5)
-    ap.add_argument("--pairs", type=int, default=5, help="image pairs cycled through the timed steps (N=1)")
+    ap.add_argument("--pairs", type=int, default=5, help="image pairs of the batch (N=1)")
+    ap.add_argument("--batch", type=int, default=1, choices=[0, 1],
+                    help="1: a step solves the image pairs concurrently (dd_run_schedule_batch); "
+                         "0: a step is one pair (they cycle)")
+    ap.add_argument("--max-inner-iter", type=int, default=100000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -319,22 +323,32 @@ def main():
 
     from ddinputs import config_images
     from paper_2001_10986_b200 import DD, SCHED_LADDER, measure_mufu_peak
+    from paper_2001_10986_b200.dd import run_schedule_batch
     w = _workload(args.config)
     n, s = w["n"], w["s"]
     eps = w["kappa_final"] / n**2
     stream = torch.cuda.Stream(dev)          # a real stream handle (the default stream is 0)
     torch.cuda.set_stream(stream)
+    # max_inner_iter: the paper gives no cap (reading A6); SPEC's 10^4
+    # is too small for cfg 5 (pair 1 has a cell needing 10 670 iterations at
+    # kappa = 0.5), so every cell runs to the P:1407-1408 stop test
     kw = dict(err_tol=w["err_tol"], trunc_tau=w["trunc_tau"], schedule=SCHED_LADDER,
-              eps_start=w["eps_start"], coarsest_side=w["coarsest"], device=local)
-    # 5 image pairs (seeds 2k+1, 2k+2), all resident in HBM; the
-    # timed steps cycle through them.  Multi-GPU: one problem striped.
+              eps_start=w["eps_start"], coarsest_side=w["coarsest"], device=local,
+              max_inner_iter=args.max_inner_iter)
+    # 5 image pairs (seeds 2k+1, 2k+2), all resident in HBM.  A
+    # step solves the batch of pairs concurrently (one context and stream per
+    # pair, dd_run_schedule_batch: one problem's cells fill the SMs another's
+    # latency-bound sweeps leave idle); --batch 0: a step is one pair.
+    # Multi-GPU: one problem striped.
     npairs = max(1, args.pairs) if world == 1 else 1
+    batched = world == 1 and args.batch == 1 and npairs > 1
+    streams = [stream] + [torch.cuda.Stream(dev) for _ in range(npairs - 1)] if batched else [stream] * npairs
     ctxs, host = [], []
     for k in range(npairs):
         mu_h, nu_h = config_images(args.config, pair=k)
         mu_d = torch.from_numpy(mu_h).to(dev)
         nu_d = torch.from_numpy(nu_h).to(dev)
-        c = DD(mu_d, nu_d, eps, s, device_input=True, stream=stream.cuda_stream, **kw)
+        c = DD(mu_d, nu_d, eps, s, device_input=True, stream=streams[k].cuda_stream, **kw)
         c._keep_host = (mu_h, nu_h)
         ctxs.append(c)
         host.append((mu_h, nu_h))
@@ -351,12 +365,22 @@ def main():
         else:
             striped.run_schedule(n, w["coarsest"], w["kappa_final"], w["eps_start"])
 
+    def reset_all(cs):
+        for c in cs:
+            c.reset()
+        for c in cs:
+            c.synchronize()
+
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    for k in range(max(args.warmup, npairs if args.warmup > 0 else 0)):
-        c = ctxs[k % npairs]
-        c.reset()
-        solve(c, run)
-        c.synchronize()
+    for k in range(args.warmup if batched else max(args.warmup, npairs if args.warmup > 0 else 0)):
+        if batched:
+            reset_all(ctxs)
+            run_schedule_batch(ctxs)
+        else:
+            c = ctxs[k % npairs]
+            c.reset()
+            solve(c, run)
+            c.synchronize()
     # ---- timed region: K steps (pair k mod 5), per-step CUDA events on the library's stream
     for c in ctxs:
         c.reset_totals()
@@ -367,11 +391,22 @@ def main():
     clocks.start()
     step_ms, cells_step, step_pair = [], [], []
     for k in range(args.steps):
-        c = ctxs[k % npairs]
         flush.fill_(1.0)                       # L2 flush between timed steps (256 MB > 126 MB L2)
-        c.reset()                              # state back to the product coupling (untimed)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        if batched:
+            reset_all(ctxs)                    # states back to the product coupling (untimed)
+            torch.cuda.synchronize(dev)
+            e0.record(stream)                  # ctxs[0]'s stream orders the batch (dd.h)
+            run_schedule_batch(ctxs)
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            step_pair.append(-1)
+            cells_step.append(None)
+            continue
+        c = ctxs[k % npairs]
+        c.reset()                              # state back to the product coupling (untimed)
         c0 = run.cells_solved if run else 0
         e0.record(stream)
         solve(c, run)
@@ -397,7 +432,27 @@ def main():
     cells_per_step = all_cells / args.steps
     value = all_cells / (wall_ms * 1e-3)
     per_pair = None
-    if run is None and npairs > 1:
+    latency = None
+    if batched:
+        # per-pair latency (time to solution of one problem alone on the GPU),
+        # outside the timed region: one dd_run_schedule per pair
+        lat = {}
+        for k, c in enumerate(ctxs):
+            c.reset()
+            c.synchronize()
+            torch.cuda.synchronize(dev)
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(streams[k])
+            c.run_schedule()
+            a1.record(streams[k])
+            a1.synchronize()
+            lat[str(k)] = a0.elapsed_time(a1)
+        v = list(lat.values())
+        latency = {"ms_per_solve": lat, "median_ms": float(np.median(v)), "sum_ms": float(np.sum(v)),
+                   "batch_speedup_vs_sequential": float(np.sum(v)) / (wall_ms / args.steps),
+                   "def": "each pair alone (dd_run_schedule), device time; the batch step solves all of them"}
+    if run is None and npairs > 1 and not batched:
         pair_rate = {}
         for k in range(npairs):
             ms = [m for m, q in zip(step_ms, step_pair) if q == k]
@@ -436,11 +491,17 @@ def main():
         prof_traffic, traffic_unit = pj.get("bytes_per_launch"), pj.get("unit")
     except Exception:
         pass
+    if batched:
+        # several problems' K1 launches overlap: take the whole step (device time)
+        k1_ms = my_ms
+        achieved = tot["mufu_ops"] / (k1_ms * 1e-3)
     roofline = {"bound": "alu", "pipe": "MUFU/XU ex2+log (SFU)", "achieved": achieved / 1e12,
                 "peak": peak / 1e12, "unit": "Top/s", "frac": achieved / peak,
                 "peak_source": "measured ex2.approx microbenchmark on this B200 (dd_measure_mufu_peak)",
                 "peak_nominal": nominal / 1e12, "traffic": prof_traffic, "traffic_unit": traffic_unit,
-                "kernel": "k1_cell_solve", "kernel_share_of_step": k1_ms / my_ms,
+                "kernel": "k1_cell_solve" + (" (all tiers; the batch's problems in flight at once: "
+                                             "algorithmic MUFU ops of the step / step device time)" if batched else ""),
+                "kernel_share_of_step": k1_ms / my_ms,
                 "mufu_ops_per_step": tot["mufu_ops"] / args.steps}
     finest = None
     if run is None:
@@ -448,7 +509,32 @@ def main():
 
     # ---- end to end through the public API with host buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and batched:
+        # the batch through the public API: dd_init from pinned host buffers,
+        # dd_run_schedule_batch, per pair dd_primal_cost + dd_marginal_error (the
+        # results read back), dd_free
+        pinned = [(torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory()) for a, b in host]
+        e2e_ms = []
+        for k in range(2):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            ges = [DD(a.numpy(), b.numpy(), eps, s, stream=streams[i].cuda_stream, **kw)
+                   for i, (a, b) in enumerate(pinned)]
+            run_schedule_batch(ges)
+            res = [(ge.primal_cost(), ge.marginal_error()) for ge in ges]
+            dt = time.perf_counter() - t0
+            for ge in ges:
+                ge.close()
+            assert all(r[1][0] <= w["err_tol"] for r in res)
+            if k > 0:
+                e2e_ms.append(dt * 1e3)
+        e2e_ms_med = float(np.median(e2e_ms))
+        e2e = {"value": cells_per_step / (e2e_ms_med * 1e-3),
+               "unit": UNIT, "h2d_bytes_per_step": int(sum(a.nbytes + b.nbytes for a, b in host)),
+               "d2h_bytes_per_step": 4 * 8 * npairs, "ms_per_step": e2e_ms_med,
+               "path": f"per pair dd_init(host buffers); dd_run_schedule_batch ({npairs} pairs); per pair "
+                       "dd_primal_cost + dd_marginal_error; dd_free"}
+    elif not args.no_e2e:
         mu_h, nu_h = host[0]
         mu_p = torch.from_numpy(mu_h).pin_memory()
         nu_p = torch.from_numpy(nu_h).pin_memory()
@@ -494,10 +580,14 @@ def main():
                             "balance and marginal sums",
             "data": "synthetic",
             "config": {**{k: w[k] for k in ("workload", "n", "s", "kappa_final", "err_tol", "trunc_tau")},
-                       "image_pairs": npairs, "global_batch": 1,
+                       "image_pairs": npairs, "global_batch": npairs if batched else 1,
+                       "step": (f"one batch: the {npairs} image pairs solved concurrently (dd_run_schedule_batch, "
+                                "one context + stream each)") if batched else "one image pair (pairs cycle)",
+                       "max_inner_iter": args.max_inner_iter,
                        "parallelism": f"stripes{world} (NCCL send/recv of boundary rows)" if world > 1 else "single",
                        "l2": "flushed between steps (256 MB write); nu_i pool > L2"},
-            "time_to_solution_ms": wall_ms / args.steps,
+            "time_to_solution_ms": latency["median_ms"] if latency else wall_ms / args.steps,
+            "latency": latency,
             "cells_per_step": cells_per_step,
             "iters_per_cell": tot["iters_sum"] / max(1, tot["cells"]),
             "pairs": per_pair, "finest_sweep": finest,

@@ -85,7 +85,15 @@ typedef struct {                /* zero-initialised fields take the defaults */
                                    [1] > 0: box-side cap of the 3-CTA/SM fused tier (tier 1);
                                    testing knobs that route cells to the other K1 tiers;
                                    [2] = 1: cold-start potentials at dd_refine (reading A14)
-                                   instead of the glued + interpolated warm start */
+                                   instead of the glued + interpolated warm start;
+                                   [3] K1 cluster tier (one cell on a cluster of CTAs, DSMEM):
+                                   0 / -1 off (default), 2 auto (the sweep's long poles), 1 every
+                                   cell of the fused big-cell path (testing); results are
+                                   bit-identical whichever tier solves a cell;
+                                   [4] > 0: cluster routing threshold theta in % (default 300:
+                                   predicted work >= theta * sweep work / #SMs);
+                                   [5] > 0: persistent clusters (default 6, capped by
+                                   cudaOccupancyMaxActiveClusters) */
 } dd_options;
 
 typedef struct {                /* one sweep (or accumulated totals) */
@@ -101,7 +109,8 @@ typedef struct {                /* one sweep (or accumulated totals) */
     long long launches;         /* kernel launches issued */
     long long big_cells;        /* cells routed to the large-box path */
     int max_box;                /* largest composite Y-box side seen */
-    int reserved_i;
+    int reserved_i;             /* outputs recomputed with an exact max (speculative misses) */
+    long long cluster_cells;    /* cells solved by the K1 cluster tier (a subset of big_cells) */
 } dd_sweep_stats;
 
 typedef struct {
@@ -147,6 +156,20 @@ int dd_refine(dd_ctx* ctx);
  * Y-feasible), DD_ENOMEM on a pool overflow. */
 int dd_run_schedule(dd_ctx* ctx);
 
+/* dd_run_schedule_batch -- dd_run_schedule on n independent problems at once
+ * (e.g. the image pairs of a batch; every context LADDER mode with the same
+ * grid side, cell size, coarsest side and final eps, on the same device, each
+ * with its OWN stream).  The sweeps are enqueued round-robin over the
+ * contexts, so the cells of one problem fill the SMs that another problem's
+ * latency-bound sweeps (a sweep lasts as long as its slowest cell) leave idle;
+ * every problem's arithmetic is unchanged (its state is bit-identical to
+ * dd_run_schedule's).  Ordering: work queued on ctxs[0]'s stream before the
+ * call precedes every context's first sweep, and ctxs[0]'s stream waits for
+ * every context's last sweep.  Waits once at the end; returns the first
+ * non-zero code of the contexts' dd_synchronize (DD_ENOCONV, DD_ENOMEM) or
+ * DD_EINVAL if the contexts do not match. */
+int dd_run_schedule_batch(dd_ctx* const* ctxs, int n);
+
 /* dd_reset -- return to the initial state (coarsest layer, product coupling). */
 int dd_reset(dd_ctx* ctx);
 
@@ -185,10 +208,13 @@ int dd_reset_totals(dd_ctx* ctx);
 
 /* dd_get_cell_stats -- per composite cell of the last sweep (cell index =
  * row-major over the partition's cell grid): Sinkhorn iterations, union
- * Y-box side max(b_r, b_c), MUFU ops of the solve and its duration on its SM
- * in units of 1024 cycles.  Any output may be NULL.  Returns the number of
- * cells (<= max_cells are written), or < 0 on error (-DD_E*). */
-int dd_get_cell_stats(dd_ctx* ctx, int* iters, int* box_side, double* mufu_ops, int* kcycles, int max_cells);
+ * Y-box side max(b_r, b_c), MUFU ops of the solve, its duration on its SM
+ * in units of 1024 cycles and its flags (bit 0: max_inner_iter reached, bit 1:
+ * non-finite value / numerically empty kernel row, bit 2: eps raised by the
+ * safeguard, bit 3: pool overflow).  Any output may be NULL.  Returns the
+ * number of cells (<= max_cells are written), or < 0 on error (-DD_E*). */
+int dd_get_cell_stats(dd_ctx* ctx, int* iters, int* box_side, double* mufu_ops, int* kcycles, int* flags,
+                      int max_cells);
 
 /* ---- multi-GPU stripes ----
  * One context per rank holds the whole layer but solves only the composite

@@ -49,6 +49,7 @@ typedef struct {                /* = dd_sweep_stats */
     double ms, mufu_ops, solve_ms;
     long long launches, big_cells;
     int max_box, reserved_i;
+    long long cluster_cells;    /* GPU cluster tier only: always 0 here */
 } shim_stats;
 
 typedef struct {                /* = dd_state_info */

@@ -11,6 +11,7 @@ struct DevStats {
     long long fallbacks, deferred, huge;
     int max_box, overflow;
     long long entries;
+    long long cluster;     // cells solved by the cluster tier
 };
 
 struct EvalParams {
@@ -37,6 +38,9 @@ struct EvalParams {
 cudaError_t k1_phase_read(unsigned long long* out32);
 size_t k1_smem_bytes_host(int s, int bcap, bool big = false, int nwarps = 0);
 cudaError_t launch_k1(const SweepParams& p, int tier, int grid, size_t smem, cudaStream_t st);
+int k1_max_clusters(size_t smem);
+cudaError_t launch_k0_cluster(const int* sorted, int* counts, int ncap, const int* bside, float theta, int nsm,
+                              int mode, int* list3, cudaStream_t st);
 cudaError_t launch_k0(const SweepParams& p, int b0, int b1, int* lists, int* counts, int ncap, int* bside,
                       int* sorted, cudaStream_t st);
 cudaError_t launch_pool2x2(const double* fine, double* coarse, int sc, cudaStream_t st);

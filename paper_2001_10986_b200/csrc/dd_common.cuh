@@ -21,6 +21,11 @@ constexpr int kT1Threads = DD_T1_NT, kT1PerSM = DD_T1_MINB;
 #define DD_T2_NT 768
 #endif
 constexpr int kT2Threads = DD_T2_NT;
+// K1 cluster tier (tier 3): tier 2's CTA shape, kClusterSize CTAs (SMs) per cell
+#ifndef DD_CLUSTER
+#define DD_CLUSTER 8
+#endif
+constexpr int kClusterSize = DD_CLUSTER;
 
 
 // ------------------------------------------------------------ constants --
@@ -100,6 +105,64 @@ __device__ __forceinline__ float rcpf(float x) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// ------------------------------------------- thread-block cluster (DSMEM) --
+// The K1 cluster tier splits one composite cell
+// over CS CTAs of a cluster: every CTA keeps a full replica of the O(a b)
+// SMEM state and each output a CTA computes is stored to all replicas.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// address of the same SMEM location in the CTA of cluster rank r
+__device__ __forceinline__ unsigned mapa_u32(unsigned a, unsigned r) {
+    unsigned o;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(o) : "r"(a), "r"(r));
+    return o;
+}
+__device__ __forceinline__ void st_cl(unsigned a, float2 v) {
+    asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ void st_cl(unsigned a, float v) {
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_cl(unsigned a, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_cl(unsigned a, int v) {
+    asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ int atom_add_cl(unsigned a, int v) {
+    int o;
+    asm volatile("atom.shared::cluster.add.u32 %0, [%1], %2;" : "=r"(o) : "r"(a), "r"(v) : "memory");
+    return o;
+}
+__device__ __forceinline__ void atom_or_cl(unsigned a, int v) {
+    asm volatile("red.shared::cluster.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+// all threads of all CTAs of the cluster; release/acquire at cluster scope
+// (orders the DSMEM stores and the global-slice writes of the iteration)
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Store v at p in this CTA and in the CS - 1 peer replicas.
+template <int CS, typename T>
+__device__ __forceinline__ void bcast(T* p, T v) {
+    *p = v;
+    if constexpr (CS > 1) {
+        const unsigned a = smem_u32(p), me = cluster_rank();
+#pragma unroll
+        for (unsigned r = 0; r < (unsigned)CS; ++r)
+            if (r != me) st_cl(mapa_u32(a, r), v);
+    }
+}
+template <int CS>
+__device__ __forceinline__ void cta_or_cluster_sync() {
+    if constexpr (CS > 1) cluster_sync_all();
+    else __syncthreads();
+}
+
 // Round to the 2^-8 grid without touching the XU pipe (two FADDs).
 __device__ __forceinline__ float grid8(float v) {
     return __fsub_rn(__fadd_rn(v, kGridMagic), kGridMagic);

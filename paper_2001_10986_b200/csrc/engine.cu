@@ -57,15 +57,27 @@ struct dd_ctx {
     // sweep plumbing
     unsigned long long* bump = nullptr;
     int* lists = nullptr;           // tier lists [3][ncell_max] (K0) + LPT-sorted tiers 1, 2 [2][ncell_max]
+                                    // + the cluster tier's list [ncell_max] (K0c)
     int* bside = nullptr;           // LPT sort key per cell (K0)
     int* ipred = nullptr;           // [2][ncell_max] iterations of each cell's last solve, per partition
     int ipred_layer = -1;           // layer the predictions belong to
-    int* counters = nullptr;        // [0..2] tier counts, [3..5] work counters, [6] overflow
+    int* counters = nullptr;        // [0..2] tier counts, [3..5] work counters, [6] overflow,
+                                    // [8] cluster-tier count, [9] its work counter, [10..11] sum of K0 work (u64)
     unsigned char* slices[2] = {nullptr, nullptr};   // BIG tiers: per-CTA global slices (log nu_cell, ACC)
     long long slice_bytes[2] = {0, 0};
     int slice_cap[2] = {0, 0};      // box side the slices were sized for
     int grid_t[2] = {0, 0};         // persistent grid of tiers 1, 2
     cudaStream_t st_t[2] = {nullptr, nullptr};   // tier 1 / tier 2 streams
+    // cluster tier: ncl persistent clusters of kClusterSize CTAs,
+    // one global slice per cluster, its own high-priority stream
+    int ncl = 0;
+    int cl_mode = 0;                // 0 auto (long poles), 1 every big-path cell
+    float cl_theta = 1.0f;
+    int nsm = 148;
+    unsigned char* cl_slices = nullptr;
+    cudaStream_t st_cl = nullptr;
+    cudaEvent_t ev_join_cl = nullptr;
+    cudaEvent_t ev_batch = nullptr;  // dd_run_schedule_batch fork / join
     cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
     CellOut* cellout = nullptr;
     long long* d_total = nullptr;   // [0] padded pool length, [1] entries
@@ -221,7 +233,11 @@ int check_overflow(dd_ctx* c) {
 #ifndef DD_T1_CAP
 #define DD_T1_CAP 120
 #endif
-constexpr int kCap1 = DD_T1_CAP, kCap2 = 704;   // tier-1 cap: measured best split
+constexpr int kCap1 = DD_T1_CAP, kCap2 = 704;
+#ifndef DD_NCL
+#define DD_NCL 6
+#endif
+constexpr int kDefaultClusters = DD_NCL;   // persistent clusters of the cluster tier   // tier-1 cap: measured best split
 // SMEM per CTA: 228 KB per SM shared by the resident CTAs, 1 KB reserved per CTA, ~1 KB static
 constexpr size_t kSmem1 = 233472 / kT1PerSM - 2048, kSmem2 = 220 * 1024;
 void tier_caps(int s, int opt_main, int opt_big, int* b0, int* b1, int* b2) {
@@ -271,6 +287,7 @@ int sweep(dd_ctx* c) {
     choose_caps(c, Lr.s);
     CK(cudaMemsetAsync(c->bump, 0, sizeof(unsigned long long), c->st));
     CK(cudaMemsetAsync(c->counters, 0, 6 * sizeof(int), c->st));
+    CK(cudaMemsetAsync(c->counters + 8, 0, 4 * sizeof(int), c->st));
     SweepParams p{};
     p.part = part;
     p.side = Lr.side; p.s = Lr.s; p.nb = Lr.nb; p.nca = nca; p.ncells = ncells;
@@ -299,9 +316,28 @@ int sweep(dd_ctx* c) {
     CK(cudaEventRecord(ev.e[0], c->st));
     int* sorted = c->lists + 3 * (size_t)c->ncell_max;
     CK(launch_k0(p, c->bcap_main, c->bcap_big, c->lists, c->counters, c->ncell_max, c->bside, sorted, c->st));
+    int* list3 = c->lists + 5 * (size_t)c->ncell_max;
+    if (c->ncl > 0)
+        CK(launch_k0_cluster(sorted, c->counters, c->ncell_max, c->bside, c->cl_theta, c->nsm, c->cl_mode, list3,
+                             c->st));
     CK(cudaEventRecord(c->ev_fork, c->st));
     CK(cudaStreamWaitEvent(c->st_t[0], c->ev_fork, 0));
     CK(cudaStreamWaitEvent(c->st_t[1], c->ev_fork, 0));
+    if (c->ncl > 0) {
+        // cluster tier first: its clusters need kClusterSize free SMs of a GPC at once
+        CK(cudaStreamWaitEvent(c->st_cl, c->ev_fork, 0));
+        SweepParams q = p;
+        q.bcap = c->bcap_big2;
+        q.list_in = list3; q.n_in = c->counters + 8; q.work_counter = c->counters + 9;
+        q.gscratch = c->cl_slices; q.gslice = c->slice_bytes[1];
+        slice_offsets(q);
+        const cudaError_t e3 = launch_k1(q, 3, c->ncl, c->smem_big2, c->serial ? c->st : c->st_cl);
+        if (e3 != cudaSuccess) {
+            set_err(c, "K1 cluster tier launch (%d clusters of %d, smem %zu): %s", c->ncl, kClusterSize,
+                    c->smem_big2, cudaGetErrorString(e3));
+            return DD_ECUDA;
+        }
+    }
     {   // tier 2: the largest boxes (LPT order), fused path, 768 threads, 1 CTA/SM
         SweepParams q = p;
         q.bcap = c->bcap_big2;
@@ -333,6 +369,10 @@ int sweep(dd_ctx* c) {
     CK(cudaEventRecord(c->ev_join[1], c->st_t[1]));
     CK(cudaStreamWaitEvent(c->st, c->ev_join[0], 0));
     CK(cudaStreamWaitEvent(c->st, c->ev_join[1], 0));
+    if (c->ncl > 0) {
+        CK(cudaEventRecord(c->ev_join_cl, c->st_cl));
+        CK(cudaStreamWaitEvent(c->st, c->ev_join_cl, 0));
+    }
     CK(cudaEventRecord(ev.e[1], c->st));
     // K2: deterministic compaction of the new boxes into the pool
     const int nb2 = Lr.nb * Lr.nb;
@@ -344,7 +384,7 @@ int sweep(dd_ctx* c) {
                            c->counters + 6, c->counters + 2, c->st));
     CK(cudaEventRecord(ev.e[2], c->st));
     c->pending.push_back(ev);
-    c->launches_pending += 8;
+    c->launches_pending += c->ncl > 0 ? 10 : 8;
     c->half_index++;
     c->last_part = part;
     if (c->pending.size() > 512) return harvest(c);
@@ -374,7 +414,7 @@ void free_all(dd_ctx* c) {
     }
     void* ptrs[] = {c->alphaA, c->alphaB, c->box, c->box2, c->off, c->off2, c->pool, c->scratch,
                     c->bump, c->lists, c->bside, c->ipred, c->slices[0], c->slices[1], c->counters, c->cellout, c->d_total, c->d_last, c->d_tot,
-                    c->eval_scratch, c->eval_res, c->d_sums, c->yacc, c->partial, c->d_xoff, c->glue};
+                    c->eval_scratch, c->eval_res, c->d_sums, c->yacc, c->partial, c->d_xoff, c->glue, c->cl_slices};
     for (void* q : ptrs) if (q) cudaFree(q);
     for (auto& ev : c->pending) for (int k = 0; k < 3; ++k) cudaEventDestroy(ev.e[k]);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -382,6 +422,9 @@ void free_all(dd_ctx* c) {
         if (c->ev_join[k]) cudaEventDestroy(c->ev_join[k]);
         if (c->st_t[k]) cudaStreamDestroy(c->st_t[k]);
     }
+    if (c->ev_join_cl) cudaEventDestroy(c->ev_join_cl);
+    if (c->ev_batch) cudaEventDestroy(c->ev_batch);
+    if (c->st_cl) cudaStreamDestroy(c->st_cl);
     for (auto& ev : c->free_events) for (int k = 0; k < 3; ++k) cudaEventDestroy(ev.e[k]);
     if (c->own_stream && c->st) cudaStreamDestroy(c->st);
 }
@@ -488,6 +531,7 @@ void fill_stats(const DevStats& d, dd_sweep_stats* s) {
     s->big_cells = d.deferred + d.huge;
     s->max_box = d.max_box;
     s->reserved_i = (int)std::min<long long>(d.fallbacks, 2147483647LL);
+    s->cluster_cells = d.cluster;
 }
 
 }  // namespace
@@ -651,11 +695,11 @@ int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, d
     CK(cudaMalloc(&c->scratch, (size_t)c->cap * sizeof(double)));
     CK(cudaMalloc(&c->bump, sizeof(unsigned long long)));
     c->ncell_max = (nbmax / 2 + 1) * (nbmax / 2 + 1);
-    CK(cudaMalloc(&c->lists, (size_t)5 * c->ncell_max * sizeof(int)));
+    CK(cudaMalloc(&c->lists, (size_t)6 * c->ncell_max * sizeof(int)));
     CK(cudaMalloc(&c->bside, (size_t)c->ncell_max * sizeof(int)));
     CK(cudaMalloc(&c->ipred, (size_t)2 * c->ncell_max * sizeof(int)));
-    CK(cudaMalloc(&c->counters, 8 * sizeof(int)));
-    CK(cudaMemsetAsync(c->counters, 0, 8 * sizeof(int), c->st));
+    CK(cudaMalloc(&c->counters, 16 * sizeof(int)));
+    CK(cudaMemsetAsync(c->counters, 0, 16 * sizeof(int), c->st));
     // BIG tiers: one global slice per persistent CTA holding log nu_cell
     // (b^2 float2), the phase-A stabilisers (b^2 float) and the extraction partial sums (b^2 float4), sized for
     // the largest tier capacity over the layers (box sides never exceed the side)
@@ -677,6 +721,30 @@ int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, d
     for (int k = 0; k < 2; ++k) {
         CK(cudaStreamCreateWithFlags(&c->st_t[k], cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&c->ev_join[k], cudaEventDisableTiming));
+    }
+    // cluster tier: reserved[3] = 0 / -1 off (default), 1 every big-path cell
+    // (testing), 2 auto (the long poles); reserved[4] routing threshold theta in
+    // % (default 300); reserved[5] clusters.  Off by default: measured, a
+    // cluster of 8 SMs solves a long-pole cell only 1.3-1.7x faster than one
+    // SM, and dd_run_schedule_batch fills the
+    // SMs a latency-bound sweep leaves idle at far better efficiency.
+    c->nsm = prop.multiProcessorCount;
+    c->cl_mode = c->opt.reserved[3] == 1 ? 1 : 0;
+    c->cl_theta = c->opt.reserved[4] > 0 ? 0.01f * (float)c->opt.reserved[4] : 3.0f;
+    if ((c->opt.reserved[3] == 1 || c->opt.reserved[3] == 2) && prop.major >= 9) {
+        size_t sm2 = 0;
+        for (int k = 0; k < nl; ++k)
+            sm2 = std::max(sm2, k1_smem_bytes_host(c->L[k].s, std::min(c->slice_cap[1], c->L[k].side), true,
+                                                   kT2Threads / 32));
+        const int want = c->opt.reserved[5] > 0 ? c->opt.reserved[5] : kDefaultClusters;
+        c->ncl = std::min(want, k1_max_clusters(sm2));
+    }
+    if (c->ncl > 0) {
+        CK(cudaMalloc(&c->cl_slices, (size_t)c->slice_bytes[1] * c->ncl));
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&c->st_cl, cudaStreamNonBlocking, hi));
+        CK(cudaEventCreateWithFlags(&c->ev_join_cl, cudaEventDisableTiming));
     }
     CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK(cudaMalloc(&c->cellout, (size_t)c->ncell_max * sizeof(CellOut)));
@@ -782,6 +850,65 @@ int dd_run_schedule(dd_ctx* c) {
     }
     // one wait at the end of the schedule: DD_ENOCONV if any cell hit max_inner_iter
     return dd_synchronize(c);
+}
+
+int dd_run_schedule_batch(dd_ctx* const* cs, int n) {
+    if (!cs || n <= 0) return DD_EINVAL;
+    dd_ctx* c = cs[0];
+    if (!c) return DD_EINVAL;
+    for (int i = 0; i < n; ++i) {
+        dd_ctx* q = cs[i];
+        if (!q || q->opt.schedule != DD_SCHED_LADDER || q->device != c->device || q->n_layers != c->n_layers ||
+            q->L[q->n_layers - 1].side != c->L[c->n_layers - 1].side || q->cell_size != c->cell_size ||
+            q->L[0].side != c->L[0].side || q->eps_final != c->eps_final || q->opt.eps_start != c->opt.eps_start) {
+            set_err(c, "dd_run_schedule_batch: context %d differs (ladder, device, grid, cell size, eps)", i);
+            return DD_EINVAL;
+        }
+        for (int j = 0; j < i; ++j)
+            if (cs[j] == q || cs[j]->st == q->st) {
+                set_err(c, "dd_run_schedule_batch: contexts %d and %d share a stream", j, i);
+                return DD_EINVAL;
+            }
+    }
+    CK(cudaSetDevice(c->device));
+    // fork: every context's stream waits for the work already queued on ctxs[0]'s
+    if (!c->ev_batch) CK(cudaEventCreateWithFlags(&c->ev_batch, cudaEventDisableTiming));
+    CK(cudaEventRecord(c->ev_batch, c->st));
+    for (int i = 1; i < n; ++i) CK(cudaStreamWaitEvent(cs[i]->st, c->ev_batch, 0));
+    const int nf = c->L[c->n_layers - 1].side;
+    const double kf = c->eps_final * (double)nf * nf;
+    int sides[256], sweeps[256];
+    double kap[256];
+    const int ns = std::min(256, build_schedule(nf, c->L[0].side, kf, c->opt.eps_start, sides, kap, sweeps, 256));
+    for (int k = 0; k < ns; ++k) {
+        for (int i = 0; i < n; ++i) {
+            dd_ctx* q = cs[i];
+            while (q->L[q->cur].side < sides[k]) {
+                int rc = dd_refine(q);
+                if (rc) return rc;
+            }
+            const double h = 1.0 / sides[k];
+            dd_set_eps(q, kap[k] * h * h);
+        }
+        for (int j = 0; j < sweeps[k]; ++j)
+            for (int i = 0; i < n; ++i) {
+                int rc = sweep(cs[i]);
+                if (rc) return rc;
+            }
+    }
+    // join: ctxs[0]'s stream waits for every context's last sweep
+    for (int i = 1; i < n; ++i) {
+        dd_ctx* q = cs[i];
+        if (!q->ev_batch) CK(cudaEventCreateWithFlags(&q->ev_batch, cudaEventDisableTiming));
+        CK(cudaEventRecord(q->ev_batch, q->st));
+        CK(cudaStreamWaitEvent(c->st, q->ev_batch, 0));
+    }
+    int first = DD_OK;
+    for (int i = 0; i < n; ++i) {
+        const int rc = dd_synchronize(cs[i]);
+        if (rc && !first) first = rc;
+    }
+    return first;
 }
 
 int dd_synchronize(dd_ctx* c) {
@@ -990,7 +1117,8 @@ int dd_phase_profile(dd_ctx* c, unsigned long long* out32) {
     return DD_OK;
 }
 
-int dd_get_cell_stats(dd_ctx* c, int* iters, int* box_side, double* mufu_ops, int* kcycles, int max_cells) {
+int dd_get_cell_stats(dd_ctx* c, int* iters, int* box_side, double* mufu_ops, int* kcycles, int* flags,
+                      int max_cells) {
     if (!c || max_cells < 0) return -DD_EINVAL;
     if (cudaSetDevice(c->device) != cudaSuccess) return -DD_ECUDA;
     int rc = harvest(c);
@@ -1011,6 +1139,7 @@ int dd_get_cell_stats(dd_ctx* c, int* iters, int* box_side, double* mufu_ops, in
             if (box_side) box_side[k] = h[k].box;
             if (mufu_ops) mufu_ops[k] = h[k].mufu;
             if (kcycles) kcycles[k] = h[k].pad;
+            if (flags) flags[k] = h[k].flags;
         }
     }
     return ncells;

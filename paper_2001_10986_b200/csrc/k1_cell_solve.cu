@@ -53,6 +53,7 @@ struct K1Lay {
     int2* RI;     // BIG: per Y row, the columns [lo, hi] where nu_cell > 0 (lo > hi: empty)
     int* GL;      // BIG: row groups of the fused pass, heaviest first (dynamic LPT)
     int2* GI;     // BIG: per row group, the union of its rows' non-zero column ranges
+    double* errv; // BIG: per X point, the X-error term of the current iteration [a_r][a_c]
 };
 
 // BIG mode (fused Y2+X1): G is never stored as
@@ -77,10 +78,10 @@ __host__ __device__ inline void k1_sizes(int s, int bcap, size_t* sz, bool big =
     sz[9] = 64 * 8;                                     // red
     sz[10] = big ? (size_t)nwarps * kGbufPerWarp * 8 : 0;   // gbuf
     sz[11] = big ? align16((2 * k1_ct_off(s, bcap) + 8) * 8) : 0;   // CP
-    sz[12] = big ? 16 : 0;                                           // WK
+    sz[12] = big ? 16 : 0;                                           // WK [0] groups [1] npos [2] flags [3] fallbacks
     sz[13] = big ? (size_t)A * A * 4 : 0;                            // FH
     sz[14] = big ? (size_t)A * A * 4 : 0;                            // FL
-    sz[15] = 0;                                                      // (unused)
+    sz[15] = big ? align16((size_t)A * A * 8) : 0;                   // errv
     sz[16] = big ? align16((size_t)(bcap + 1) * 8) : 0;             // RI
     sz[17] = big ? align16((size_t)(bcap / 4 + 2) * 4) : 0;         // GL
     sz[18] = 0;                                                      // (unused)
@@ -115,7 +116,7 @@ __device__ inline K1Lay k1_carve(unsigned char* base, int s, int bcap, bool big 
 
     L.FH = (float*)(base + o); o += sz[13];
     L.FL = (float*)(base + o); o += sz[14];
-    o += sz[15];
+    L.errv = (double*)(base + o); o += sz[15];
     L.RI = (int2*)(base + o); o += sz[16];
     L.GL = (int*)(base + o); o += sz[17];
     o += sz[18];
@@ -215,6 +216,9 @@ template <int PASS, int NT>
 __device__ __forceinline__ void lse_pass(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all,
                                          float2* Fcur, float2* Fout, double& err_acc, int& fallbacks,
                                          int& nonfinite) {
+    // NT threads take part (a larger block calls it with a smaller NT: the
+    // lane-group split, hence the summation order, depends on NT only)
+    if (threadIdx.x >= NT) return;
     constexpr bool kY1 = (PASS == PY1 || PASS == PY1S);
     constexpr bool kY2 = (PASS == PY2 || PASS == PY2S);
     constexpr bool kSplit = (PASS == PY1S || PASS == PY2S);
@@ -458,7 +462,7 @@ __device__ __forceinline__ void lse_pass(const K1Lay& L, const Dims& d, const Gr
 __device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
 template <bool B> struct BoolTag { static constexpr bool value = B; };
 
-template <int NT, int AR, int NQ, int RG>
+template <int NT, int AR, int NQ, int RG, int CS>
 __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all,
                                            const float2* __restrict__ LNUg, float* __restrict__ SLg,
                                            int& fallbacks, int& nonfinite) {
@@ -480,9 +484,12 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
     const float2* CP = L.CP;
 
     const int ng = (d.br + RG - 1) / RG;
+    // the group counter lives in cluster rank 0 (CS > 1: groups are dealt
+    // over all warps of the cluster)
+    const unsigned wk0 = CS > 1 ? mapa_u32(smem_u32(&L.WK[0]), 0) : 0u;
     while (true) {
         int u = 0;
-        if (lane == 0) u = atomicAdd(&L.WK[0], 1);
+        if (lane == 0) u = CS > 1 ? atom_add_cl(wk0, 1) : atomicAdd(&L.WK[0], 1);
         u = __shfl_sync(0xffffffffu, u, 0);
         if (u >= ng) break;
         const int grp = L.GL[u];
@@ -761,7 +768,7 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
                     u = make_float2(S[j] + lh, ll);
                     if (!(fabsf(u.x) < 1e30f)) nonfinite = 1;
                 }
-                L.Ut[(x2b + j) * d.pU + y1B] = u;
+                bcast<CS>(&L.Ut[(x2b + j) * d.pU + y1B], u);
             }
         }
     }
@@ -774,7 +781,7 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
 // broadcast 128-bit loads from the hi/lo planes, the per-lane cost pair
 // (C(x2 - y2), C(x2 + 1 - y2)) from CP; speculative stabiliser = previous T
 // (exact two-pass on the first iteration or when the window check fails).
-template <int NT>
+template <int NT, int CS>
 __device__ void y1_big(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all, int& fallbacks,
                        int& nonfinite) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -782,7 +789,8 @@ __device__ void y1_big(const K1Lay& L, const Dims& d, const Grid& gq, bool exact
     const int nchunks = (d.bc + 31) >> 5;
     const int nunits = nchunks * npair;
     const float2 L2E2 = make_float2(kL2E, kL2E);
-    for (int u = warp; u < nunits; u += NT / 32) {
+    const int rank = CS > 1 ? (int)cluster_rank() : 0;
+    for (int u = warp * CS + rank; u < nunits; u += CS * (NT / 32)) {
         const int c = u / npair, pr = u % npair;
         const int y2 = 32 * c + lane;
         const bool vy = y2 < d.bc;
@@ -856,83 +864,94 @@ __device__ void y1_big(const K1Lay& L, const Dims& d, const Grid& gq, bool exact
                 t1 = make_float2(S1 + lh, fmaf(-lh, kL2E, l2));
                 if (!(fabsf(t1.x) < 1e30f)) nonfinite = 1;
             }
-            Tc[x1] = t0;
-            Tc[x1 + 1] = t1;
+            bcast<CS>(&Tc[x1], t0);
+            bcast<CS>(&Tc[x1 + 1], t1);
         }
     }
 }
 
 // BIG: the X2 half-pass and the X-iteration's finalisation, after the
-// block barrier of the fused pass:
+// block (cluster) barrier of the fused pass:
 //   F_new(x1, x2) = log mu - (S + ln sum_y1 exp(U(y1, x2) - C(y1 - x1) - S))
 // with the speculative stabiliser S = LM - F (the previous X2 LSE).  A task
-// is (x1 pair, x2); P = NT / 128 threads split its rows (fixed ranges,
-// xor-tree combine: deterministic); per row one LDS.64 of U and one of the
-// cost pair feed two exps.  An output whose sum leaves [1/4, 4] is recomputed
-// with an exact max over y1.  Accumulates the L1 X-error of the plan (F, G).
-template <int P>
+// is (x1 pair, x2); P = 4 threads split its rows (fixed ranges, xor-tree
+// combine) whatever the CTA shape or cluster size, so the big-cell path's
+// result does not depend on either (tiers 1, 2 and the cluster tier agree
+// bit for bit).  Tasks go round-robin over the cluster's CTAs; per row one
+// LDS.64 of U and one of the cost pair feed two exps.  An output whose sum
+// leaves [1/4, 4] is recomputed with an exact max over y1.  Each output's
+// term of the L1 X-error of the plan (F, G) goes to errv[x] (summed in a
+// fixed order by err_sum after the barrier).
+template <int CS>
 __device__ __forceinline__ void x2_out(const K1Lay& L, const Dims& d, const Grid& gq, int h, int x1a, int x2,
                                        float2 lm0, float2 lm1, float2 fo0, float2 fo1, float S0, float S1,
-                                       float2 a, const float2* __restrict__ Ur, float2* Fout, double& err_acc,
+                                       float2 a, const float2* __restrict__ Ur, float2* Fout,
                                        int& fallbacks, int& nonfinite);
-template <int NT>
+template <int NT, int CS>
 __device__ void x2_finalize(const K1Lay& L, const Dims& d, const Grid& gq, const float2* Fcur, float2* Fout,
-                            double& err_acc, int& fallbacks, int& nonfinite) {
-    // threads per task: the largest power of two <= min(4, NT / 128) (with
-    // NT = 768 the last 256 threads idle here, with NT = 384 the last 128)
-    constexpr int P = NT >= 512 ? 4 : (NT >= 256 ? 2 : 1);
-    static_assert(P == 1 || P == 2 || P == 4, "x2 split");
-    if (threadIdx.x == 0) L.WK[0] = 0;     // unit counter of the next fused pass
-    const int t = threadIdx.x / P, h = threadIdx.x % P;
+                            int& fallbacks, int& nonfinite) {
+#ifndef DD_X2P
+#define DD_X2P 2
+#endif
+    constexpr int P = DD_X2P;
+    constexpr int SLOTS = NT / P;          // task slots per CTA
+    static_assert(NT % (32 * P) == 0 && (P == 2 || P == 4), "x2 split");
+    const int rank = CS > 1 ? (int)cluster_rank() : 0;
+    if (threadIdx.x == 0 && rank == 0) L.WK[0] = 0;     // row-group counter of the next fused pass
     const int ntask = (d.ar >> 1) * d.ac;
-    const bool tv = t < ntask;
-    const int x2 = tv ? t % d.ac : 0, x1a = tv ? 2 * (t / d.ac) : 0;
-    const float2 lm0 = L.LM[x1a * d.ac + x2], lm1 = L.LM[(x1a + 1) * d.ac + x2];
-    const float2 fo0 = Fcur[x1a * d.pX + x2], fo1 = Fcur[(x1a + 1) * d.pX + x2];
-    const float S0 = (fo0.x > -INFINITY && lm0.x > -INFINITY) ? lm0.x - fo0.x : 0.f;
-    const float S1 = (fo1.x > -INFINITY && lm1.x > -INFINITY) ? lm1.x - fo1.x : 0.f;
+    const int h = threadIdx.x % P;
     const int R = (d.br + P - 1) / P;
-    const int ya = tv ? min(h * R, d.br) : 0, yb = tv ? min(ya + R, d.br) : 0;
-    const float2* __restrict__ Ur = L.Ut + x2 * d.pU;
-    const float2* __restrict__ cpr = L.CP + d.off - x1a;     // cpr[y1] = (C(x1a - y1), C(x1a + 1 - y1))
-    const float2 nS = make_float2(-S0, -S1);
     const float2 L2E2 = make_float2(kL2E, kL2E);
-    float2 a = make_float2(0.f, 0.f), b = make_float2(0.f, 0.f);
-    auto row = [&](int yy, float2& acc) {
-        const float2 u = Ur[yy], c = cpr[yy];
-        float2 tt = __fadd2_rn(__fadd2_rn(make_float2(u.x, u.x), neg2(c)), nS);   // exact (hi grid)
-        tt = __ffma2_rn(tt, L2E2, make_float2(u.y, u.y));
-        acc = __fadd2_rn(acc, make_float2(ex2f(tt.x), ex2f(tt.y)));
-    };
-    int y = ya;
-    for (; y + 4 <= yb; y += 4) {
-        row(y, a); row(y + 1, b); row(y + 2, a); row(y + 3, b);
-    }
-    for (; y < yb; ++y) row(y, a);
-    a = __fadd2_rn(a, b);
+    for (int base = 0; base < ntask; base += CS * SLOTS) {
+        const int t = base + (threadIdx.x / P) * CS + rank;
+        const bool tv = t < ntask;
+        const int x2 = tv ? t % d.ac : 0, x1a = tv ? 2 * (t / d.ac) : 0;
+        const float2 lm0 = L.LM[x1a * d.ac + x2], lm1 = L.LM[(x1a + 1) * d.ac + x2];
+        const float2 fo0 = Fcur[x1a * d.pX + x2], fo1 = Fcur[(x1a + 1) * d.pX + x2];
+        const float S0 = (fo0.x > -INFINITY && lm0.x > -INFINITY) ? lm0.x - fo0.x : 0.f;
+        const float S1 = (fo1.x > -INFINITY && lm1.x > -INFINITY) ? lm1.x - fo1.x : 0.f;
+        const int ya = tv ? min(h * R, d.br) : 0, yb = tv ? min(ya + R, d.br) : 0;
+        const float2* __restrict__ Ur = L.Ut + x2 * d.pU;
+        const float2* __restrict__ cpr = L.CP + d.off - x1a;     // cpr[y1] = (C(x1a - y1), C(x1a + 1 - y1))
+        const float2 nS = make_float2(-S0, -S1);
+        float2 a = make_float2(0.f, 0.f), b = make_float2(0.f, 0.f);
+        auto row = [&](int yy, float2& acc) {
+            const float2 u = Ur[yy], c = cpr[yy];
+            float2 tt = __fadd2_rn(__fadd2_rn(make_float2(u.x, u.x), neg2(c)), nS);   // exact (hi grid)
+            tt = __ffma2_rn(tt, L2E2, make_float2(u.y, u.y));
+            acc = __fadd2_rn(acc, make_float2(ex2f(tt.x), ex2f(tt.y)));
+        };
+        int y = ya;
+        for (; y + 4 <= yb; y += 4) {
+            row(y, a); row(y + 1, b); row(y + 2, a); row(y + 3, b);
+        }
+        for (; y < yb; ++y) row(y, a);
+        a = __fadd2_rn(a, b);
 #pragma unroll
-    for (int o = 1; o < P; o <<= 1) {
-        a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
-        a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+        for (int o = 1; o < P; o <<= 1) {
+            a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
+            a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+        }
+        // lane h < 2 finalises output (x1a + h, x2)
+        if (tv && h < 2)
+            x2_out<CS>(L, d, gq, h, x1a, x2, lm0, lm1, fo0, fo1, S0, S1, a, Ur, Fout, fallbacks, nonfinite);
     }
-    if (!tv || h >= 2) return;
-    // lane h finalises output (x1a + h, x2) (P = 1: both)
-    for (int hh = h; hh < 2; hh += (P == 1 ? 1 : 2)) x2_out<P>(L, d, gq, hh, x1a, x2, lm0, lm1, fo0, fo1, S0, S1, a,
-                                                             Ur, Fout, err_acc, fallbacks, nonfinite);
 }
 
-template <int P>
+template <int CS>
 __device__ __forceinline__ void x2_out(const K1Lay& L, const Dims& d, const Grid& gq, int h, int x1a, int x2,
                                        float2 lm0, float2 lm1, float2 fo0, float2 fo1, float S0, float S1,
-                                       float2 a, const float2* __restrict__ Ur, float2* Fout, double& err_acc,
+                                       float2 a, const float2* __restrict__ Ur, float2* Fout,
                                        int& fallbacks, int& nonfinite) {
     const int x1 = x1a + h, o = x1 * d.ac + x2;
     const float2 lm = h ? lm1 : lm0;
     const float2 fo = h ? fo1 : fo0;
+    float2* fp = &Fout[x1 * d.pX + x2];
     if (lm.x == -INFINITY) {
-        Fout[x1 * d.pX + x2] = make_float2(-INFINITY, 0.f);
-        L.FH[o] = -INFINITY;
-        L.FL[o] = 0.f;
+        bcast<CS>(fp, make_float2(-INFINITY, 0.f));
+        bcast<CS>(&L.FH[o], -INFINITY);
+        bcast<CS>(&L.FL[o], 0.f);
+        bcast<CS>(&L.errv[o], 0.0);
         return;
     }
     float S = h ? S1 : S0;
@@ -953,34 +972,43 @@ __device__ __forceinline__ void x2_out(const K1Lay& L, const Dims& d, const Grid
     }
     if (!(s > 1e-37f) || !(S > -INFINITY)) {
         nonfinite = 1;
-        Fout[x1 * d.pX + x2] = make_float2(-INFINITY, 0.f);
-        L.FH[o] = -INFINITY;
-        L.FL[o] = 0.f;
+        bcast<CS>(fp, make_float2(-INFINITY, 0.f));
+        bcast<CS>(&L.FH[o], -INFINITY);
+        bcast<CS>(&L.FL[o], 0.f);
+        bcast<CS>(&L.errv[o], 0.0);
         return;
     }
     float lh, ll;
     ln_split(s, gq, lh, ll);
     const float2 fn = make_float2(lm.x - (S + lh), lm.y - ll);
-    Fout[x1 * d.pX + x2] = fn;
-    L.FH[o] = fn.x;
-    L.FL[o] = fn.y;
+    bcast<CS>(fp, fn);
+    bcast<CS>(&L.FH[o], fn.x);
+    bcast<CS>(&L.FL[o], fn.y);
     if (!(fabsf(fn.x) < 1e30f)) nonfinite = 1;
     // P_X pi(x) = mu(x) exp(F - F_new)  (plan (F, G))
     const float dF = (fo.x - fn.x) + (fo.y - fn.y) * kLN2;
-    err_acc += (double)L.MU[o] * (double)fabsf(expm1f(dF));
+    bcast<CS>(&L.errv[o], (double)L.MU[o] * (double)fabsf(expm1f(dF)));
 }
 
-template <int NT>
+// Fixed-order sum of the per-output X-error terms (every warp computes it;
+// the xor butterfly gives identical bits in every lane, warp and CTA).
+__device__ __forceinline__ double err_sum(const double* ev, int n) {
+    double v = 0.0;
+    for (int k = threadIdx.x & 31; k < n; k += 32) v += ev[k];
+    return warp_sum(v);
+}
+
+template <int NT, int CS>
 __device__ void fused_dispatch(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all,
                                const float2* LNUg, float* SLg, int& fb, int& nf) {
     // row groups of RG = 4 (measured: RG = 2 loses more to per-group overhead
     // than it gains in last-round balance; RG = 8 the reverse)
     if (d.ar > 8) {
-        if (d.ac > 8) fused_y2x1<NT, 16, 4, 4>(L, d, gq, exact_all, LNUg, SLg, fb, nf);
-        else fused_y2x1<NT, 16, 2, 4>(L, d, gq, exact_all, LNUg, SLg, fb, nf);
+        if (d.ac > 8) fused_y2x1<NT, 16, 4, 4, CS>(L, d, gq, exact_all, LNUg, SLg, fb, nf);
+        else fused_y2x1<NT, 16, 2, 4, CS>(L, d, gq, exact_all, LNUg, SLg, fb, nf);
     } else {
-        if (d.ac > 8) fused_y2x1<NT, 8, 4, 4>(L, d, gq, exact_all, LNUg, SLg, fb, nf);
-        else fused_y2x1<NT, 8, 2, 4>(L, d, gq, exact_all, LNUg, SLg, fb, nf);
+        if (d.ac > 8) fused_y2x1<NT, 8, 4, 4, CS>(L, d, gq, exact_all, LNUg, SLg, fb, nf);
+        else fused_y2x1<NT, 8, 2, 4, CS>(L, d, gq, exact_all, LNUg, SLg, fb, nf);
     }
 }
 
@@ -1013,9 +1041,17 @@ __device__ void final_split_big(const K1Lay& L, const Dims& d, float4* __restric
 }
 
 // ----------------------------------------------------------- the solve --
-template <int NT, bool BIG>
+// CS > 1 (cluster tier, BIG only): the CS CTAs of a cluster solve the cell
+// together: each keeps a replica of the SMEM state,
+// Y1 units, fused row groups and X2 tasks are dealt over the cluster and
+// every output is stored to all replicas (DSMEM); three cluster barriers per
+// iteration.  Rank 0 alone runs the extraction and the epilogue.  gslice is
+// the cluster's (shared) global slice.
+template <int NT, bool BIG, int CS>
 __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, unsigned char* gslice) {
+    static_assert(CS == 1 || BIG, "cluster tier = big-cell path");
     const K1Lay L = k1_carve(base, p.s, p.bcap, BIG, NT / 32);
+    const int rank = CS > 1 ? (int)cluster_rank() : 0;
     __shared__ int4 s_box[4];
     __shared__ long long s_off[4];
     __shared__ int s_q[4];          // quadrant of each member
@@ -1120,7 +1156,24 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     const double lambda = block_max(fmax_l, L.red);
     const double fmin_b = -block_max(-fmin_l, L.red + 16);
     const double frange = (lambda > fmin_b) ? lambda - fmin_b : 0.0;
-    muJ = block_sum(muJ, L.red + 32);
+    if (BIG) {
+        // ||mu_J|| in a fixed order (one warp), so that the stop tolerance of
+        // the big-cell path does not depend on the CTA shape
+        if (tid < 32) {
+            double v = 0.0;
+            for (int x = tid; x < nx; x += 32) {
+                int xr, xc;
+                goff(x / d.ac, x % d.ac, xr, xc);
+                v += p.mu[(long long)(R0 + xr) * p.side + (C0 + xc)];
+            }
+            v = warp_sum(v);
+            if (tid == 0) L.red[60] = v;
+        }
+        __syncthreads();
+        muJ = L.red[60];
+    } else {
+        muJ = block_sum(muJ, L.red + 32);
+    }
     // ---- per-cell hi grid: magnitudes bounded by M = 2 Cmax + 2 |F| + 64
     Grid gq;
     {
@@ -1160,7 +1213,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     float4* ACCp = BIG ? reinterpret_cast<float4*>(gslice + p.acc_off) : reinterpret_cast<float4*>(L.G);
     const int ny = d.br * d.bc;
     double npos = 0.0;
-    for (int y = tid; y < ny; y += NT) {
+    for (int y = rank * NT + tid; y < ny; y += CS * NT) {
         int gy, gx;
         goff(y / d.bc, y % d.bc, gy, gx);
         gy += Y0;
@@ -1175,6 +1228,12 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         npos += (v > 0.0) ? 1.0 : 0.0;
     }
     npos = block_sum(npos, L.red);     // (barrier: staging complete)
+    if constexpr (CS > 1) {
+        // the slice rows of the other CTAs; the non-zero count at rank 0
+        if (tid == 0) atom_add_cl(mapa_u32(smem_u32(&L.WK[1]), 0), (int)npos);
+        cluster_sync_all();
+        npos = (double)L.WK[1];
+    }
     if (BIG) {
         // per Y row: the non-zero columns of nu_cell.  The separable passes
         // only need those (G = -inf elsewhere); about half of a union box is
@@ -1227,27 +1286,35 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         const bool exact = (it == 0);
         double e_loc = 0.0;
         PROF_T(ta);
-        if (BIG) y1_big<NT>(L, d, gq, exact, fallbacks, nonfinite);
+        if (BIG) y1_big<NT, CS>(L, d, gq, exact, fallbacks, nonfinite);
         else lse_pass<PY1, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
         PROF_T(tb);
-        __syncthreads();
+        cta_or_cluster_sync<CS>();
         PROF_T(tc);
         if (BIG) {
-            fused_dispatch<NT>(L, d, gq, exact, LNU, SLg, fallbacks, nonfinite);
+            fused_dispatch<NT, CS>(L, d, gq, exact, LNU, SLg, fallbacks, nonfinite);
         } else {
             lse_pass<PY2, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
             __syncthreads();
             lse_pass<PX1, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
         }
         PROF_T(td);
-        __syncthreads();
+        cta_or_cluster_sync<CS>();
         PROF_T(te);
-        if (BIG) x2_finalize<NT>(L, d, gq, Fc, Fn, e_loc, fallbacks, nonfinite);
-        else lse_pass<PX2, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
+        if (BIG) {
+            x2_finalize<NT, CS>(L, d, gq, Fc, Fn, fallbacks, nonfinite);
+        } else {
+            lse_pass<PX2, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
+        }
         PROF_T(tf);
-        // one barrier: the previous iteration's reads of red[] are two
-        // barriers back (after Y1, after the Y2/X1 passes)
-        err = block_sum1(e_loc, L.red);
+        if (BIG) {
+            cta_or_cluster_sync<CS>();
+            err = err_sum(L.errv, nx);
+        } else {
+            // one barrier: the previous iteration's reads of red[] are two
+            // barriers back (after Y1, after the Y2/X1 passes)
+            err = block_sum1(e_loc, L.red);
+        }
         PROF_T(tg);
         // per warp: busy time of the passes and barrier waits (phase profile build only)
         PROF_ADD(0, tb - ta); PROF_ADD(1, tc - tb); PROF_ADD(2, td - tc); PROF_ADD(3, te - td);
@@ -1260,17 +1327,31 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     PROF_T(t_loop1);
     PROF_ADD(6, t_loop1 - t_loop0);
     PROF_ADD(7, t_loop0 - t_start);
+    int peer_fallbacks = 0;
+    if constexpr (CS > 1) {
+        // flags and fallback counts of the other CTAs to rank 0, which alone
+        // runs the extraction and the epilogue (its replica is complete)
+        const int fb = (int)block_sum((double)fallbacks, L.red + 32);
+        if (rank != 0) {
+            if (nonfinite) atom_or_cl(mapa_u32(smem_u32(&s_flag), 0), 2);
+            if (tid == 0) atom_add_cl(mapa_u32(smem_u32(&L.WK[3]), 0), fb);
+        }
+        cluster_sync_all();
+        if (rank != 0) return;
+        peer_fallbacks = L.WK[3];
+    }
     // ---- line 10: extraction from the plan (F, G): exact Y-iteration with
     // the row sums split by basic-cell quadrant (x1 half, x2 half)
     {
         double dummy = 0.0;
-        lse_pass<PY1S, NT>(L, d, gq, true, Fc, Fn, dummy, fallbacks, nonfinite);
+        // (the big-cell path: 256 threads, whatever the CTA shape)
+        lse_pass<PY1S, BIG ? 256 : NT>(L, d, gq, true, Fc, Fn, dummy, fallbacks, nonfinite);
         __syncthreads();
         if (BIG) final_split_big<NT>(L, d, ACCp);
         else lse_pass<PY2S, NT>(L, d, gq, true, Fc, Fn, dummy, fallbacks, nonfinite);
     }
     if (nonfinite) atomicOr(&s_flag, 2);
-    fallbacks = (int)block_sum((double)fallbacks, L.red + 32);
+    fallbacks = (int)block_sum((double)fallbacks, L.red + 32) + peer_fallbacks;
     co.flags |= s_flag;
     co.iters = it;
     if (tid == 0 && p.ipred) p.ipred[cell] = it;
@@ -1304,7 +1385,9 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     };
     // line 10: nu_i(y) = nu_cell(y) S_i(y) / S(y) (ratio form, A7); norms
     double nrm0 = 0.0, nrm1 = 0.0, nrm2 = 0.0, nrm3 = 0.0;
-    for (int y = tid; y < ny; y += NT) {
+    // (the big-cell path: 256 threads in a fixed order, whatever the CTA shape)
+    constexpr int NTN = BIG ? 256 : NT;
+    for (int y = tid; y < ny && tid < NTN; y += NTN) {
         const float4 a = ACC[y];
         const double tot = (double)a.x + (double)a.y + (double)a.z + (double)a.w;
         if (!(tot > 0.0)) continue;
@@ -1444,23 +1527,45 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
 
 // Persistent CTAs pulling cells from a tier list (K0 classification).
 // BIG = false: all per-cell arrays in SMEM (small Y boxes, 3 CTAs/SM);
-// BIG = true: fused Y2+X1 path, O(a b) SMEM + a global slice per CTA.
-template <int NT, bool BIG, int MINB>
+// BIG = true: fused Y2+X1 path, O(a b) SMEM + a global slice per CTA;
+// CS > 1: persistent clusters of CS CTAs, one cell per cluster at a time,
+// one global slice per cluster.
+template <int NT, bool BIG, int MINB, int CS>
 __global__ void __launch_bounds__(NT, MINB) k1_cell_solve(SweepParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_cell;
     unsigned char* base = smem;
-    unsigned char* gslice = BIG ? p.gscratch + (long long)blockIdx.x * p.gslice : nullptr;
-    while (true) {
-        if (threadIdx.x == 0) {
-            const int k = atomicAdd(p.work_counter, 1);
-            s_cell = (k < *p.n_in) ? p.list_in[k] : -1;
+    const int slot = CS > 1 ? blockIdx.x / CS : blockIdx.x;
+    unsigned char* gslice = BIG ? p.gscratch + (long long)slot * p.gslice : nullptr;
+    if constexpr (CS == 1) {
+        while (true) {
+            if (threadIdx.x == 0) {
+                const int k = atomicAdd(p.work_counter, 1);
+                s_cell = (k < *p.n_in) ? p.list_in[k] : -1;
+            }
+            __syncthreads();
+            const int cell = s_cell;
+            if (cell < 0) return;
+            solve_cell<NT, BIG, 1>(p, cell, base, gslice);
+            __syncthreads();
         }
-        __syncthreads();
-        const int cell = s_cell;
-        if (cell < 0) return;
-        solve_cell<NT, BIG>(p, cell, base, gslice);
-        __syncthreads();
+    } else {
+        const K1Lay L = k1_carve(base, p.s, p.bcap, BIG, NT / 32);
+        const unsigned rank = cluster_rank();
+        while (true) {
+            if (rank == 0 && threadIdx.x == 0) {
+                const int k = atomicAdd(p.work_counter, 1);
+                const int c = (k < *p.n_in) ? p.list_in[k] : -1;
+                L.WK[1] = 0;          // the cell's cluster counters (non-zero count, fallbacks)
+                L.WK[3] = 0;
+                for (unsigned r = 0; r < (unsigned)CS; ++r) st_cl(mapa_u32(smem_u32(&s_cell), r), c);
+            }
+            cluster_sync_all();
+            const int cell = s_cell;
+            if (cell < 0) return;        // all CTAs of the cluster leave together
+            solve_cell<NT, BIG, CS>(p, cell, base, gslice);
+            cluster_sync_all();          // rank 0's epilogue done before the next cell's stores
+        }
     }
 }
 
@@ -1468,7 +1573,8 @@ __global__ void __launch_bounds__(NT, MINB) k1_cell_solve(SweepParams p) {
 // (tier 0 <= b0: SMEM path; tier 1 <= b1 and tier 2 (beyond): BIG path;
 // cells beyond tier 2's capacity are flagged by the solve), and record the
 // side for the LPT ordering of the big tiers.
-__global__ void k0_classify(SweepParams p, int b0, int b1, int* lists, int* counts, int ncap, int* bside) {
+__global__ void k0_classify(SweepParams p, int b0, int b1, int* lists, int* counts, int ncap, int* bside,
+                            unsigned long long* wsum) {
     const int cell = blockIdx.x * blockDim.x + threadIdx.x;
     if (cell >= p.ncells) return;
     const int cp = cell / p.nca, cq = cell % p.nca;
@@ -1500,6 +1606,42 @@ __global__ void k0_classify(SweepParams p, int b0, int b1, int* lists, int* coun
     const int ip = p.ipred ? max(1, p.ipred[cell]) : 1;
     const float w = (float)max(bmax, 1) * (float)max(bmax, 1) * (float)ip;
     bside[cell] = min(1023, (int)(32.f * __log2f(w)));
+    atomicAdd(wsum, (unsigned long long)max(bmax, 1) * (unsigned long long)max(bmax, 1) * (unsigned long long)ip);
+}
+
+// K0c: route the long poles of the sweep to the cluster tier.  A cell whose
+// predicted work w (box area x previous iterations, the K0 key) exceeds
+// theta x (the sweep's total predicted work) / #SMs would run longer on one
+// SM than the whole sweep takes when spread over the machine.  The big tiers'
+// LPT lists are sorted by the key, so the long poles are their prefixes: the
+// cluster list merges the two prefixes (largest first) and tiers 1 / 2 start
+// their work counters behind them.  mode 1: every big-path cell (testing).
+// The big-path result does not depend on the tier (x2_finalize), so the
+// routing only affects timing.
+__global__ void k0_cluster(const int* sorted, int* counts, int ncap, const int* bside,
+                           const unsigned long long* wsum, float theta, int nsm, int mode, int* list3) {
+    if (threadIdx.x != 0) return;
+    const int n1 = counts[1], n2 = counts[2];
+    const int* l1 = sorted;
+    const int* l2 = sorted + ncap;
+    int thr = 1 << 30;
+    if (mode == 1) {
+        thr = -1;
+    } else {
+        const double w = (double)*wsum * (double)theta / (double)nsm;
+        if (w >= 1.0) thr = (int)(32.0 * log2(w));
+    }
+    int a = 0, b = 0;
+    while (a < n1 && bside[l1[a]] >= thr) ++a;
+    while (b < n2 && bside[l2[b]] >= thr) ++b;
+    int i = 0, j = 0, k = 0;
+    while (i < b || j < a) {      // merge, tier-2 (larger box) first on equal keys
+        if (j >= a || (i < b && bside[l2[i]] >= bside[l1[j]])) list3[k++] = l2[i++];
+        else list3[k++] = l1[j++];
+    }
+    counts[8] = k;                 // cluster tier: list length, work counter counts[9] (zeroed)
+    counts[4] = a;                 // tier 1 starts behind its prefix
+    counts[5] = b;                 // tier 2 likewise
 }
 
 // LPT order for the big tiers: counting sort of the tier-t list by the K0
@@ -1539,18 +1681,26 @@ cudaError_t k1_phase_read(unsigned long long* out32) {
 #endif
 }
 
+cudaError_t launch_k0_cluster(const int* sorted, int* counts, int ncap, const int* bside, float theta, int nsm,
+                              int mode, int* list3, cudaStream_t st) {
+    k0_cluster<<<1, 32, 0, st>>>(sorted, counts, ncap, bside, reinterpret_cast<const unsigned long long*>(counts + 10),
+                                 theta, nsm, mode, list3);
+    return cudaGetLastError();
+}
+
 size_t k1_smem_bytes_host(int s, int bcap, bool big, int nwarps) { return k1_smem_bytes(s, bcap, big, nwarps); }
 
 cudaError_t launch_k0(const SweepParams& p, int b0, int b1, int* lists, int* counts, int ncap, int* bside,
                       int* sorted, cudaStream_t st) {
-    k0_classify<<<(p.ncells + 255) / 256, 256, 0, st>>>(p, b0, b1, lists, counts, ncap, bside);
+    k0_classify<<<(p.ncells + 255) / 256, 256, 0, st>>>(p, b0, b1, lists, counts, ncap, bside,
+                                                         reinterpret_cast<unsigned long long*>(counts + 10));
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     k0_sort<<<2, 1024, 0, st>>>(lists, counts, ncap, bside, sorted);
     return cudaGetLastError();
 }
 
-template <int NT, bool BIG, int MINB>
+template <int NT, bool BIG, int MINB, int CS>
 static cudaError_t launch_tier(const SweepParams& p, int grid, size_t smem, cudaStream_t st) {
     // the SMEM opt-in is a per-device function attribute: cache it per device
     static size_t attr[64] = {0};
@@ -1561,20 +1711,64 @@ static cudaError_t launch_tier(const SweepParams& p, int grid, size_t smem, cuda
     // opt in whenever the request grows: the 48 KB default covers static +
     // dynamic SMEM together, so a dynamic size just under 48 KB can fail too
     if (smem > attr[dev]) {
-        e = cudaFuncSetAttribute(k1_cell_solve<NT, BIG, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = cudaFuncSetAttribute(k1_cell_solve<NT, BIG, MINB, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr[dev] = smem;
     }
-    k1_cell_solve<NT, BIG, MINB><<<grid, NT, smem, st>>>(p);
-    return cudaGetLastError();
+    if constexpr (CS == 1) {
+        k1_cell_solve<NT, BIG, MINB, CS><<<grid, NT, smem, st>>>(p);
+        return cudaGetLastError();
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid * CS);
+        cfg.blockDim = dim3(NT);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = CS;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, k1_cell_solve<NT, BIG, MINB, CS>, p);
+    }
 }
 
 // tier 0: 256 threads, all arrays in SMEM, 3 CTAs/SM;
-// tier 1: BIG path, 256 threads, 3 CTAs/SM; tier 2: BIG path, 768 threads, 1 CTA/SM (both <= 80 registers).
+// tier 1: BIG path, 256 threads, 3 CTAs/SM; tier 2: BIG path, 768 threads, 1 CTA/SM (both <= 80 registers);
+// tier 3 (cluster tier): tier 2's CTA in clusters of kClusterSize, grid = number of clusters.
 cudaError_t launch_k1(const SweepParams& p, int tier, int grid, size_t smem, cudaStream_t st) {
-    if (tier == 0) return launch_tier<256, false, DD_T0_MINB>(p, grid, smem, st);
-    if (tier == 1) return launch_tier<kT1Threads, true, kT1PerSM>(p, grid, smem, st);
-    return launch_tier<kT2Threads, true, 1>(p, grid, smem, st);
+    if (tier == 0) return launch_tier<256, false, DD_T0_MINB, 1>(p, grid, smem, st);
+    if (tier == 1) return launch_tier<kT1Threads, true, kT1PerSM, 1>(p, grid, smem, st);
+    if (tier == 2) return launch_tier<kT2Threads, true, 1, 1>(p, grid, smem, st);
+    return launch_tier<kT2Threads, true, 1, kClusterSize>(p, grid, smem, st);
+}
+
+// Clusters of the cluster tier that can be resident at once (0: none).
+int k1_max_clusters(size_t smem) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kClusterSize * 32);
+    cfg.blockDim = dim3(kT2Threads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kClusterSize;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaFuncSetAttribute(k1_cell_solve<kT2Threads, true, 1, kClusterSize>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k1_cell_solve<kT2Threads, true, 1, kClusterSize>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
 }
 
 }  // namespace dd

@@ -157,6 +157,7 @@ __global__ void k_reduce_stats(const CellOut* __restrict__ out, int ncells, DevS
         L.fallbacks = s_fb[0];
         L.deferred = *n_deferred;
         L.huge = *n_huge;
+        L.cluster = n_huge[6];             // counters[8]: the cluster tier's list length
         L.max_box = s_box[0];
         L.overflow = *overflow;
         L.entries = *entries;
@@ -170,6 +171,7 @@ __global__ void k_reduce_stats(const CellOut* __restrict__ out, int ncells, DevS
         tot->fallbacks += L.fallbacks;
         tot->deferred += L.deferred;
         tot->huge += L.huge;
+        tot->cluster += L.cluster;
         tot->max_box = max(tot->max_box, L.max_box);
         tot->overflow |= L.overflow;
         tot->entries = L.entries;

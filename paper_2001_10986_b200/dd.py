@@ -21,7 +21,7 @@ FLAG_DEVICE_INPUT = 1
 PLAN_BASIC_MARGINALS, PLAN_COO = 0, 1
 
 # every symbol include/dd.h declares (checked by tests/test_abi.py)
-EXPORTS = ["dd_init", "dd_iterate", "dd_set_eps", "dd_refine", "dd_run_schedule", "dd_reset",
+EXPORTS = ["dd_init", "dd_iterate", "dd_set_eps", "dd_refine", "dd_run_schedule", "dd_run_schedule_batch", "dd_reset",
            "dd_primal_cost", "dd_dual_gap", "dd_marginal_error", "dd_fetch_plan", "dd_get_stats", "dd_get_totals",
            "dd_reset_totals", "dd_set_stripe", "dd_clear_rows", "dd_export_rows",
            "dd_import_rows", "dd_copy_alpha", "dd_y_accumulate", "dd_y_l1", "dd_phase_profile", "dd_get_cell_stats", "dd_get_state_info", "dd_get_state", "dd_set_state",
@@ -47,7 +47,7 @@ class SweepStats(C.Structure):
                 ("failed", C.c_int), ("err_x_sum", C.c_double), ("entries", C.c_longlong),
                 ("ms", C.c_double), ("mufu_ops", C.c_double), ("solve_ms", C.c_double),
                 ("launches", C.c_longlong), ("big_cells", C.c_longlong), ("max_box", C.c_int),
-                ("reserved_i", C.c_int)]
+                ("reserved_i", C.c_int), ("cluster_cells", C.c_longlong)]
 
 
 class StateInfo(C.Structure):
@@ -72,6 +72,8 @@ def lib():
         L.dd_set_eps.argtypes = [p, d]
         L.dd_refine.argtypes = [p]
         L.dd_run_schedule.argtypes = [p]
+        if hasattr(L, "dd_run_schedule_batch"):     # (older A/B variant builds lack it)
+            L.dd_run_schedule_batch.argtypes = [C.POINTER(C.c_void_p), C.c_int]
         L.dd_reset.argtypes = [p]
         L.dd_primal_cost.argtypes = [p, C.POINTER(d), C.POINTER(d)]
         L.dd_marginal_error.argtypes = [p, C.POINTER(d), C.POINTER(d)]
@@ -80,7 +82,7 @@ def lib():
         L.dd_get_stats.argtypes = [p, C.POINTER(SweepStats)]
         L.dd_get_totals.argtypes = [p, C.POINTER(SweepStats)]
         L.dd_reset_totals.argtypes = [p]
-        L.dd_get_cell_stats.argtypes = [p, p, p, p, p, i]
+        L.dd_get_cell_stats.argtypes = [p, p, p, p, p, p, i]
         L.dd_phase_profile.argtypes = [p, p]
         L.dd_set_stripe.argtypes = [p, i, i]
         L.dd_clear_rows.argtypes = [p, i, i]
@@ -122,13 +124,24 @@ def measure_mufu_peak(device=0):
     return v.value
 
 
+def run_schedule_batch(dds):
+    """dd_run_schedule_batch: the full schedule of several independent problems
+    (contexts on distinct streams), sweeps enqueued round-robin, one wait."""
+    arr = (C.c_void_p * len(dds))(*[d._h.value for d in dds])
+    rc = lib().dd_run_schedule_batch(arr, len(dds))
+    if rc != OK:
+        return dds[0]._check(rc, "run_schedule_batch")
+    return rc
+
+
 class DD:
     """One libdd_gpu context.  Same call names as the oracle's binding."""
 
     def __init__(self, mu, nu, eps, cell_size, *, err_tol=1e-6, trunc_tau=1e-15,
                  max_inner_iter=10000, schedule=SCHED_FIXED, eps_start=0.0, coarsest_side=8,
                  no_truncate=False, device=0, pool_capacity=0, stream=None, device_input=False,
-                 bcap_main=0, bcap_big=0, cold_refine=False, check_every=1):
+                 bcap_main=0, bcap_big=0, cold_refine=False, check_every=1, cluster=0,
+                 cluster_theta=0, n_clusters=0):
         opt = Options()
         opt.err_tol = err_tol
         opt.trunc_tau = trunc_tau
@@ -144,6 +157,9 @@ class DD:
         opt.reserved[0] = bcap_main
         opt.reserved[1] = bcap_big
         opt.reserved[2] = 1 if cold_refine else 0
+        opt.reserved[3] = cluster            # K1 cluster tier: 0 off, 2 auto (long poles), 1 every big-path cell
+        opt.reserved[4] = cluster_theta      # routing threshold in % (0 -> default)
+        opt.reserved[5] = n_clusters         # persistent clusters (0 -> default)
         self._h = C.c_void_p()
         if device_input:
             # mu, nu: objects exposing data_ptr() (device fp64) and a square shape
@@ -188,8 +204,8 @@ class DD:
     def set_eps(self, eps):
         return self._check(lib().dd_set_eps(self._h, eps), "set_eps")
 
-    def iterate(self, k=1):
-        return self._check(lib().dd_iterate(self._h, k), "iterate")
+    def iterate(self, k=1, check=True):
+        return self._check(lib().dd_iterate(self._h, k), "iterate", (OK,) if check else (OK, ENOCONV))
 
     def refine(self):
         return self._check(lib().dd_refine(self._h), "refine")
@@ -200,8 +216,8 @@ class DD:
     def reset(self):
         return self._check(lib().dd_reset(self._h), "reset")
 
-    def synchronize(self):
-        return self._check(lib().dd_synchronize(self._h), "synchronize")
+    def synchronize(self, check=True):
+        return self._check(lib().dd_synchronize(self._h), "synchronize", (OK,) if check else (OK, ENOCONV))
 
     def primal_cost(self):
         a, b = C.c_double(), C.c_double()
@@ -275,16 +291,20 @@ class DD:
         self._check(lib().dd_phase_profile(self._h, out.ctypes.data), "phase_profile")
         return out.reshape(2, 16)
 
-    def cell_stats(self):
-        """Per composite cell of the last sweep: (iters, box_side, mufu_ops, kcycles) arrays."""
-        n = lib().dd_get_cell_stats(self._h, None, None, None, None, 0)
+    def cell_stats(self, flags=False):
+        """Per composite cell of the last sweep: (iters, box_side, mufu_ops, kcycles[, flags]) arrays."""
+        n = lib().dd_get_cell_stats(self._h, None, None, None, None, None, 0)
         if n < 0:
             raise RuntimeError(f"dd_get_cell_stats rc={-n}: {self.last_error()}")
         it = np.zeros(max(n, 1), np.int32)
         bx = np.zeros(max(n, 1), np.int32)
         mf = np.zeros(max(n, 1), np.float64)
         kc = np.zeros(max(n, 1), np.int32)
-        lib().dd_get_cell_stats(self._h, it.ctypes.data, bx.ctypes.data, mf.ctypes.data, kc.ctypes.data, n)
+        fl = np.zeros(max(n, 1), np.int32)
+        lib().dd_get_cell_stats(self._h, it.ctypes.data, bx.ctypes.data, mf.ctypes.data, kc.ctypes.data,
+                                fl.ctypes.data, n)
+        if flags:
+            return it[:n], bx[:n], mf[:n], kc[:n], fl[:n]
         return it[:n], bx[:n], mf[:n], kc[:n]
 
     def state_info(self):

@@ -33,7 +33,7 @@ class Stats(C.Structure):
                 ("failed", C.c_int), ("err_x_sum", C.c_double), ("entries", C.c_longlong),
                 ("ms", C.c_double), ("mufu_ops", C.c_double), ("solve_ms", C.c_double),
                 ("launches", C.c_longlong), ("big_cells", C.c_longlong), ("max_box", C.c_int),
-                ("reserved_i", C.c_int)]
+                ("reserved_i", C.c_int), ("cluster_cells", C.c_longlong)]
 
 
 class Info(C.Structure):

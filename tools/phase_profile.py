@@ -17,6 +17,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--cfg", type=int, default=5)
 ap.add_argument("--min-side", type=int, default=1024)
 ap.add_argument("--build-only", action="store_true")
+ap.add_argument("--cluster", type=int, default=0, help="dd_options.reserved[3] (1: every big-path cell on the cluster tier)")
 a = ap.parse_args()
 
 if a.build_only:
@@ -34,14 +35,14 @@ p = CONFIGS[a.cfg]
 n, s = p["n"], p["s"]
 mu, nu = config_images(a.cfg)
 g = DD(mu, nu, p["kappa_final"] / n**2, s, schedule=1, coarsest_side=p.get("coarsest", 8),
-       eps_start=p.get("eps_start", 0.0))
+       eps_start=p.get("eps_start", 0.0), max_inner_iter=100000, cluster=a.cluster)
 names = ["Y1", "bar1", "Y2X1", "bar2", "X2", "errsum", "loop", "prologue", "epilogue(cta)", "iters(cta)"]
 for side, kappa, sweeps in build_schedule(n, p.get("coarsest", 8), p["kappa_final"], p.get("eps_start", 0.0)):
     while g.state_info()["side"] < side:
         g.refine()
     g.set_eps(kappa / side**2)
     g.phase_profile()
-    g.iterate(sweeps)
+    g.iterate(sweeps, check=False)
     pp = g.phase_profile().astype(np.float64)
     if side < a.min_side:
         continue

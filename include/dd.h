@@ -143,6 +143,10 @@ int dd_iterate(dd_ctx* ctx, int n_half_iters);
 /* dd_set_eps -- change eps keeping alpha = eps log u constant. */
 int dd_set_eps(dd_ctx* ctx, double eps);
 
+/* dd_set_max_inner_iter -- the Sinkhorn iteration cap of the following sweeps
+ * (dd_options.max_inner_iter; reading A6).  k >= 1, else DD_EINVAL. */
+int dd_set_max_inner_iter(dd_ctx* ctx, int k);
+
 /* dd_refine -- move to the next finer layer: nu_i^0 by eq. FineBasicMarginals
  * (P:1471-1474); alpha warm start = the coarse potentials glued by the
  * discrete Helmholtz least squares and interpolated linearly in
@@ -211,10 +215,12 @@ int dd_reset_totals(dd_ctx* ctx);
  * Y-box side max(b_r, b_c), MUFU ops of the solve, its duration on its SM
  * in units of 1024 cycles and its flags (bit 0: max_inner_iter reached, bit 1:
  * non-finite value / numerically empty kernel row, bit 2: eps raised by the
- * safeguard, bit 3: pool overflow).  Any output may be NULL.  Returns the
- * number of cells (<= max_cells are written), or < 0 on error (-DD_E*). */
+ * safeguard, bit 3: pool overflow) and the L1 X-error of its returned plan
+ * as K1 evaluated it (relative to 1, not to ||mu_J||).  Any output may
+ * be NULL.  Returns the number of cells (<= max_cells are written), or < 0 on
+ * error (-DD_E*). */
 int dd_get_cell_stats(dd_ctx* ctx, int* iters, int* box_side, double* mufu_ops, int* kcycles, int* flags,
-                      int max_cells);
+                      float* err_x, int max_cells);
 
 /* ---- multi-GPU stripes ----
  * One context per rank holds the whole layer but solves only the composite

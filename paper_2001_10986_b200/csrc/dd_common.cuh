@@ -82,6 +82,8 @@ struct SweepParams {
     int* work_counter;    // modes 1/2 dynamic work index
     int* overflow;        // set if scratch capacity exceeded
     int* ipred;           // this partition's iteration counts of the previous sweep (work predictor for the LPT order)
+    int poison;           // testing (DD_POISON): K1 fills its dynamic SMEM with 0xFF bytes first
+    size_t smem_bytes;    // dynamic SMEM of the launch (for the poison fill)
 };
 
 // ------------------------------------------------------------- helpers --

@@ -78,6 +78,7 @@ struct dd_ctx {
     cudaStream_t st_cl = nullptr;
     cudaEvent_t ev_join_cl = nullptr;
     cudaEvent_t ev_batch = nullptr;  // dd_run_schedule_batch fork / join
+    int poison = 0;                 // DD_POISON (testing): poisoned buffers and K1 SMEM
     cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
     CellOut* cellout = nullptr;
     long long* d_total = nullptr;   // [0] padded pool length, [1] entries
@@ -304,6 +305,7 @@ int sweep(dd_ctx* c) {
     p.mu = Lr.mu; p.logmu = Lr.logmu; p.mass_i = Lr.mass;
     p.out = c->cellout;
     p.overflow = c->counters + 6;
+    p.poison = c->poison;
     // work predictor for the LPT order (order only: results do not depend on it)
     if (c->ipred_layer != c->cur) {
         CK(cudaMemsetAsync(c->ipred, 0, (size_t)2 * c->ncell_max * sizeof(int), c->st));
@@ -762,6 +764,26 @@ int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, d
     CK(cudaMemsetAsync(c->d_last, 0, sizeof(DevStats), c->st));
     CK(cudaMemsetAsync(c->d_tot, 0, sizeof(DevStats), c->st));
     CK(cudaMemsetAsync(c->d_total, 0, 2 * sizeof(long long), c->st));
+    // DD_POISON=1 (testing): fill the state and scratch buffers with 0xFF
+    // (NaN) bytes and have K1 poison its SMEM, so that a read of memory the
+    // path did not write shows up as a result difference (tests/test_batch_gpu.py)
+    if (getenv("DD_POISON")) {
+        c->poison = 1;
+        const size_t nbm = (size_t)nbmax * nbmax;
+        CK(cudaMemsetAsync(c->pool, 0xFF, (size_t)c->cap * sizeof(double), c->st));
+        CK(cudaMemsetAsync(c->scratch, 0xFF, (size_t)c->cap * sizeof(double), c->st));
+        CK(cudaMemsetAsync(c->box, 0xFF, nbm * sizeof(int4), c->st));
+        CK(cudaMemsetAsync(c->box2, 0xFF, nbm * sizeof(int4), c->st));
+        CK(cudaMemsetAsync(c->off, 0xFF, nbm * sizeof(long long), c->st));
+        CK(cudaMemsetAsync(c->off2, 0xFF, nbm * sizeof(long long), c->st));
+        CK(cudaMemsetAsync(c->alphaA, 0xFF, n2 * sizeof(double), c->st));
+        CK(cudaMemsetAsync(c->alphaB, 0xFF, n2 * sizeof(double), c->st));
+        for (int t = 0; t < 2; ++t)
+            CK(cudaMemsetAsync(c->slices[t], 0xFF, (size_t)c->slice_bytes[t] * c->grid_t[t], c->st));
+        if (c->cl_slices) CK(cudaMemsetAsync(c->cl_slices, 0xFF, (size_t)c->slice_bytes[1] * c->ncl, c->st));
+        CK(cudaMemsetAsync(c->cellout, 0xFF, (size_t)c->ncell_max * sizeof(CellOut), c->st));
+        CK(cudaMemsetAsync(c->yacc, 0xFF, n2 * sizeof(unsigned long long), c->st));
+    }
     // K1 needs > 48 KB dynamic SMEM on the big path: set the attribute once here
     choose_caps(c, F.s);
     c->cur = 0;
@@ -780,6 +802,12 @@ int dd_reset(dd_ctx* c) {
     c->stripe_lo = c->stripe_hi = 0;
     c->eps = (c->opt.schedule == DD_SCHED_LADDER) ? 2.0 / ((double)c->L[0].side * c->L[0].side) : c->eps_final;
     return product_init(c);
+}
+
+int dd_set_max_inner_iter(dd_ctx* c, int k) {
+    if (!c || k < 1) return DD_EINVAL;
+    c->opt.max_inner_iter = k;
+    return DD_OK;
 }
 
 int dd_set_eps(dd_ctx* c, double eps) {
@@ -1118,7 +1146,7 @@ int dd_phase_profile(dd_ctx* c, unsigned long long* out32) {
 }
 
 int dd_get_cell_stats(dd_ctx* c, int* iters, int* box_side, double* mufu_ops, int* kcycles, int* flags,
-                      int max_cells) {
+                      float* err_x, int max_cells) {
     if (!c || max_cells < 0) return -DD_EINVAL;
     if (cudaSetDevice(c->device) != cudaSuccess) return -DD_ECUDA;
     int rc = harvest(c);
@@ -1140,6 +1168,7 @@ int dd_get_cell_stats(dd_ctx* c, int* iters, int* box_side, double* mufu_ops, in
             if (mufu_ops) mufu_ops[k] = h[k].mufu;
             if (kcycles) kcycles[k] = h[k].pad;
             if (flags) flags[k] = h[k].flags;
+            if (err_x) err_x[k] = h[k].err;
         }
     }
     return ncells;

@@ -81,7 +81,7 @@ __host__ __device__ inline void k1_sizes(int s, int bcap, size_t* sz, bool big =
     sz[12] = big ? 16 : 0;                                           // WK [0] groups [1] npos [2] flags [3] fallbacks
     sz[13] = big ? (size_t)A * A * 4 : 0;                            // FH
     sz[14] = big ? (size_t)A * A * 4 : 0;                            // FL
-    sz[15] = big ? align16((size_t)A * A * 8) : 0;                   // errv
+    sz[15] = align16((size_t)A * A * 8);                             // errv (fp64 rescue, BIG loop)
     sz[16] = big ? align16((size_t)(bcap + 1) * 8) : 0;             // RI
     sz[17] = big ? align16((size_t)(bcap / 4 + 2) * 4) : 0;         // GL
     sz[18] = 0;                                                      // (unused)
@@ -558,7 +558,9 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
 #pragma unroll 4
             for (int x = 0; x < AR; ++x) {
                 float2 t = Tc[x];
-                if (AR == 8) t.x = (x < d.ar) ? t.x : -INFINITY;     // s = 4 edge cells (a_r = 4)
+                // s = 4 edge cells (a_r = 4): rows x >= a_r are past T's pitch
+                // (stale SMEM): both halves replaced, so no NaN / inf leaks in
+                if (AR == 8 && x >= d.ar) t = make_float2(-INFINITY, 0.f);
 #pragma unroll
                 for (int i = 0; i < NP; ++i) {
                     const float2 cs = __fadd2_rn(cpb[x - 2 * i], neg2(nS[i]));   // C + S (exact)
@@ -1040,6 +1042,109 @@ __device__ void final_split_big(const K1Lay& L, const Dims& d, float4* __restric
     }
 }
 
+// ------------------------------------------------------- fp64 rescue --
+// A cell whose fp32 X-error stalls just above its tolerance (measured: the
+// error floor of the fp32 passes can reach ~1.04 ||mu_J|| Err on cells of
+// tiny mass next to the image border, where the fp64 oracle converges in a
+// few hundred iterations) continues from its current potentials with the
+// same four separable log-domain passes in fp64 (exact max stabilisers,
+// libm exp/log) until err <= tol.  Every output is computed by one thread
+// of a fixed set of 256 (NT-independent, deterministic); Y potentials and
+// log nu_cell in fp64 live in G64 / LNU64.  Returns the iterations done;
+// F holds the plan's F (F_old of the last iteration) as fp64 on return.
+// (the paper's safeguard for cells the fast
+// solver cannot finish is Sec. 7.3.)
+constexpr int kRescueIters = 2048;
+
+template <int NT>
+__device__ int rescue_fp64(const K1Lay& L, const Dims& d, double* F, double* Fn, double* G64, int gstr,
+                           const double* LNU64, int lstr, double inv_kappa, double tol, int max_it, double& err) {
+    constexpr int NR = 256;
+    const int tid = threadIdx.x;
+    const bool act = tid < NR;
+    double* T = reinterpret_cast<double*>(L.Tt);     // [y2][pT]
+    double* U = reinterpret_cast<double*>(L.Ut);     // [x2][pU]
+    auto C = [inv_kappa](int k) { const double v = (double)k; return v * v * inv_kappa; };
+    int n = 0;
+    while (true) {
+        // Y1: T(x1, y2) = LSE_x2 [F(x1, x2) - C(x2 - y2)]
+        for (int o = tid; act && o < d.ar * d.bc; o += NR) {
+            const int x1 = o % d.ar, y2 = o / d.ar;
+            const double* Fr = F + x1 * d.pX;
+            double M = -INFINITY;
+            for (int x2 = 0; x2 < d.ac; ++x2) M = fmax(M, Fr[x2] - C(x2 - y2));
+            double sm = 0.0;
+            if (M > -INFINITY)
+                for (int x2 = 0; x2 < d.ac; ++x2) sm += exp(Fr[x2] - C(x2 - y2) - M);
+            T[y2 * d.pT + x1] = M > -INFINITY ? M + log(sm) : -INFINITY;
+        }
+        __syncthreads();
+        // Y2: G(y1, y2) = log nu_cell - LSE_x1 [T(x1, y2) - C(x1 - y1)]
+        for (int o = tid; act && o < d.br * d.bc; o += NR) {
+            const int y1 = o / d.bc, y2 = o % d.bc;
+            const double ln = LNU64[(size_t)o * lstr];
+            double g = -INFINITY;
+            if (ln > -INFINITY) {
+                const double* Tc = T + y2 * d.pT;
+                double M = -INFINITY;
+                for (int x1 = 0; x1 < d.ar; ++x1) M = fmax(M, Tc[x1] - C(x1 - y1));
+                double sm = 0.0;
+                for (int x1 = 0; x1 < d.ar; ++x1) sm += exp(Tc[x1] - C(x1 - y1) - M);
+                g = ln - (M + log(sm));
+            }
+            G64[(size_t)o * gstr] = g;
+        }
+        __syncthreads();
+        // X1: U(y1, x2) = LSE_y2 [G(y1, y2) - C(y2 - x2)]
+        for (int o = tid; act && o < d.br * d.ac; o += NR) {
+            const int y1 = o % d.br, x2 = o / d.br;
+            const double* Gr = G64 + (size_t)y1 * d.bc * gstr;
+            double M = -INFINITY;
+            for (int y2 = 0; y2 < d.bc; ++y2) M = fmax(M, Gr[(size_t)y2 * gstr] - C(y2 - x2));
+            double sm = 0.0;
+            if (M > -INFINITY)
+                for (int y2 = 0; y2 < d.bc; ++y2) sm += exp(Gr[(size_t)y2 * gstr] - C(y2 - x2) - M);
+            U[x2 * d.pU + y1] = M > -INFINITY ? M + log(sm) : -INFINITY;
+        }
+        __syncthreads();
+        // X2: F_new = log mu - LSE_y1 [U(y1, x2) - C(y1 - x1)]; X-error of the plan (F, G)
+        for (int o = tid; act && o < d.ar * d.ac; o += NR) {
+            const int x1 = o / d.ac, x2 = o % d.ac;
+            const float2 lmf = L.LM[o];
+            const double lm = lmf.x == -INFINITY ? -INFINITY : join_hl(lmf);
+            double fn = -INFINITY, e = 0.0;
+            if (lm > -INFINITY) {
+                const double* Ur = U + x2 * d.pU;
+                double M = -INFINITY;
+                for (int y1 = 0; y1 < d.br; ++y1) M = fmax(M, Ur[y1] - C(y1 - x1));
+                double sm = 0.0;
+                if (M > -INFINITY)
+                    for (int y1 = 0; y1 < d.br; ++y1) sm += exp(Ur[y1] - C(y1 - x1) - M);
+                fn = M > -INFINITY ? lm - (M + log(sm)) : -INFINITY;
+                const double f = F[x1 * d.pX + x2];
+                e = (fn > -INFINITY && f > -INFINITY) ? (double)L.MU[o] * fabs(expm1(f - fn)) : 0.0;
+            }
+            Fn[x1 * d.pX + x2] = fn;
+            L.errv[o] = e;
+        }
+        __syncthreads();
+        err = err_sum(L.errv, d.ar * d.ac);
+        ++n;
+        if (err <= tol || n >= max_it || !(err == err)) break;
+        __syncthreads();      // every warp has read errv before the next X2 writes it
+        double* t = F; F = Fn; Fn = t;
+    }
+    // the plan's F (F_old) into the first buffer for the caller
+    if (n % 2 == 0) {
+        for (int o = tid; o < d.ar * d.ac; o += NT) {
+            const int i = (o / d.ac) * d.pX + o % d.ac;
+            Fn[i] = F[i];
+        }
+        __syncthreads();
+    }
+    return n;
+}
+
 // ----------------------------------------------------------- the solve --
 // CS > 1 (cluster tier, BIG only): the CS CTAs of a cluster solve the cell
 // together: each keeps a replica of the SMEM state,
@@ -1276,11 +1381,26 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     // stop at err <= (1 - 2^-7) ||mu_J|| Err: the test runs on the fp32
     // potentials; the margin keeps the fp64 re-evaluation of the plan's
     // X-error (dd_marginal_error) within P:1409's bound (A28)
+    auto nucell = [&](int y) {
+        int gy, gx;
+        goff(y / d.bc, y % d.bc, gy, gx);
+        gy += Y0;
+        gx += X0;
+        double v = 0.0;
+        for (int m = 0; m < nmem; ++m) {
+            const int4 b = s_box[m];
+            const int ry = gy - b.x, rx = gx - b.y;
+            if (ry >= 0 && ry < b.z && rx >= 0 && rx < b.w) v += p.pool_in[s_off[m] + (long long)ry * b.w + rx];
+        }
+        return v;
+    };
     const double tol = muJ * p.err_tol * (1.0 - 0.0078125);
     float2* Fc = L.FX;
     float2* Fn = L.FXn;
     int it = 0, fallbacks = 0, nonfinite = 0;
     double err = 0.0;
+    double err_ck = INFINITY;       // X-error at the last stall checkpoint
+    bool rescue = false;
     PROF_T(t_loop0);
     while (true) {
         const bool exact = (it == 0);
@@ -1322,6 +1442,12 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         ++it;
         if (err <= tol && it % p.check_every == 0) break;
         if (it >= p.max_iter || !(err == err)) { co.flags |= 1; break; }
+        // stall at the fp32 error floor: < 2 % progress over 256 iterations
+        // within 1.5x of the tolerance -> continue in fp64 (rescue_fp64)
+        if ((it & 255) == 0) {
+            if (it >= 512 && err < 1.5 * tol && err > 0.98 * err_ck) { rescue = true; break; }
+            err_ck = err;
+        }
         float2* t = Fc; Fc = Fn; Fn = t;
     }
     PROF_T(t_loop1);
@@ -1339,6 +1465,50 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         cluster_sync_all();
         if (rank != 0) return;
         peer_fallbacks = L.WK[3];
+    }
+    if (rescue) {
+        // fp64 continuation (rescue_fp64): potentials and Y-side arrays as fp64
+        double* F64 = reinterpret_cast<double*>(Fc);
+        double* Fn64 = reinterpret_cast<double*>(Fn);
+        for (int x = tid; x < nx; x += NT) {
+            const int i = (x / d.ac) * d.pX + x % d.ac;
+            const float2 f = Fc[i];
+            F64[i] = f.x == -INFINITY ? -INFINITY : join_hl(f);
+        }
+        double* G64;
+        double* LNU64;
+        int str;
+        if (BIG) {
+            G64 = reinterpret_cast<double*>(ACCp);
+            LNU64 = G64 + 1;
+            str = 2;
+        } else {
+            G64 = reinterpret_cast<double*>(L.G);
+            LNU64 = reinterpret_cast<double*>(L.LNU);
+            str = 1;
+        }
+        for (int y = tid; y < ny; y += NT) {
+            const double v = nucell(y);
+            LNU64[(size_t)y * str] = v > 0.0 ? log(v) : -INFINITY;
+        }
+        __syncthreads();
+        double e64 = err;
+        // at most kRescueIters fp64 iterations: a precision stall converges in a
+        // few hundred (measured 257); a cell that is merely this slow in fp64
+        // too (the oracle needs > 4e4 iterations on such cells) keeps its
+        // Y-feasible plan and is flagged (reading A6)
+        const int n = rescue_fp64<NT>(L, d, F64, Fn64, G64, str, LNU64, str, inv_kappa, tol,
+                                      max(1, min(kRescueIters, p.max_iter - it)), e64);
+        it += n;
+        err = e64;
+        co.flags |= 16;                       // solved to the tolerance by the fp64 rescue
+        if (!(err <= tol)) co.flags |= 1;
+        for (int x = tid; x < nx; x += NT) {
+            const int i = (x / d.ac) * d.pX + x % d.ac;
+            const double f = F64[i];
+            Fc[i] = split_hl(f, gq);
+        }
+        __syncthreads();
     }
     // ---- line 10: extraction from the plan (F, G): exact Y-iteration with
     // the row sums split by basic-cell quadrant (x1 half, x2 half)
@@ -1370,19 +1540,6 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
 
     // ---- epilogue (ACC over the G+LNU region; nu_cell re-gathered from pool_in)
     const float4* ACC = ACCp;
-    auto nucell = [&](int y) {
-        int gy, gx;
-        goff(y / d.bc, y % d.bc, gy, gx);
-        gy += Y0;
-        gx += X0;
-        double v = 0.0;
-        for (int m = 0; m < nmem; ++m) {
-            const int4 b = s_box[m];
-            const int ry = gy - b.x, rx = gx - b.y;
-            if (ry >= 0 && ry < b.z && rx >= 0 && rx < b.w) v += p.pool_in[s_off[m] + (long long)ry * b.w + rx];
-        }
-        return v;
-    };
     // line 10: nu_i(y) = nu_cell(y) S_i(y) / S(y) (ratio form, A7); norms
     double nrm0 = 0.0, nrm1 = 0.0, nrm2 = 0.0, nrm3 = 0.0;
     // (the big-cell path: 256 threads in a fixed order, whatever the CTA shape)
@@ -1537,6 +1694,10 @@ __global__ void __launch_bounds__(NT, MINB) k1_cell_solve(SweepParams p) {
     unsigned char* base = smem;
     const int slot = CS > 1 ? blockIdx.x / CS : blockIdx.x;
     unsigned char* gslice = BIG ? p.gscratch + (long long)slot * p.gslice : nullptr;
+    if (p.poison) {     // testing: SMEM the path did not write reads as NaN
+        for (size_t i = threadIdx.x; i < p.smem_bytes / 4; i += NT) reinterpret_cast<unsigned*>(smem)[i] = 0xFFFFFFFFu;
+        __syncthreads();
+    }
     if constexpr (CS == 1) {
         while (true) {
             if (threadIdx.x == 0) {
@@ -1715,8 +1876,10 @@ static cudaError_t launch_tier(const SweepParams& p, int grid, size_t smem, cuda
         if (e != cudaSuccess) return e;
         attr[dev] = smem;
     }
+    SweepParams q = p;
+    q.smem_bytes = smem;
     if constexpr (CS == 1) {
-        k1_cell_solve<NT, BIG, MINB, CS><<<grid, NT, smem, st>>>(p);
+        k1_cell_solve<NT, BIG, MINB, CS><<<grid, NT, smem, st>>>(q);
         return cudaGetLastError();
     } else {
         cudaLaunchConfig_t cfg = {};
@@ -1731,7 +1894,7 @@ static cudaError_t launch_tier(const SweepParams& p, int grid, size_t smem, cuda
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        return cudaLaunchKernelEx(&cfg, k1_cell_solve<NT, BIG, MINB, CS>, p);
+        return cudaLaunchKernelEx(&cfg, k1_cell_solve<NT, BIG, MINB, CS>, q);
     }
 }
 

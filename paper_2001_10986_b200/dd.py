@@ -21,7 +21,7 @@ FLAG_DEVICE_INPUT = 1
 PLAN_BASIC_MARGINALS, PLAN_COO = 0, 1
 
 # every symbol include/dd.h declares (checked by tests/test_abi.py)
-EXPORTS = ["dd_init", "dd_iterate", "dd_set_eps", "dd_refine", "dd_run_schedule", "dd_run_schedule_batch", "dd_reset",
+EXPORTS = ["dd_init", "dd_iterate", "dd_set_eps", "dd_set_max_inner_iter", "dd_refine", "dd_run_schedule", "dd_run_schedule_batch", "dd_reset",
            "dd_primal_cost", "dd_dual_gap", "dd_marginal_error", "dd_fetch_plan", "dd_get_stats", "dd_get_totals",
            "dd_reset_totals", "dd_set_stripe", "dd_clear_rows", "dd_export_rows",
            "dd_import_rows", "dd_copy_alpha", "dd_y_accumulate", "dd_y_l1", "dd_phase_profile", "dd_get_cell_stats", "dd_get_state_info", "dd_get_state", "dd_set_state",
@@ -70,6 +70,8 @@ def lib():
         L.dd_init.argtypes = [C.POINTER(p), i, p, p, i, d, i, C.POINTER(Options)]
         L.dd_iterate.argtypes = [p, i]
         L.dd_set_eps.argtypes = [p, d]
+        if hasattr(L, "dd_set_max_inner_iter"):
+            L.dd_set_max_inner_iter.argtypes = [p, i]
         L.dd_refine.argtypes = [p]
         L.dd_run_schedule.argtypes = [p]
         if hasattr(L, "dd_run_schedule_batch"):     # (older A/B variant builds lack it)
@@ -82,7 +84,7 @@ def lib():
         L.dd_get_stats.argtypes = [p, C.POINTER(SweepStats)]
         L.dd_get_totals.argtypes = [p, C.POINTER(SweepStats)]
         L.dd_reset_totals.argtypes = [p]
-        L.dd_get_cell_stats.argtypes = [p, p, p, p, p, p, i]
+        L.dd_get_cell_stats.argtypes = [p, p, p, p, p, p, p, i]
         L.dd_phase_profile.argtypes = [p, p]
         L.dd_set_stripe.argtypes = [p, i, i]
         L.dd_clear_rows.argtypes = [p, i, i]
@@ -204,6 +206,9 @@ class DD:
     def set_eps(self, eps):
         return self._check(lib().dd_set_eps(self._h, eps), "set_eps")
 
+    def set_max_inner_iter(self, k):
+        return self._check(lib().dd_set_max_inner_iter(self._h, k), "set_max_inner_iter")
+
     def iterate(self, k=1, check=True):
         return self._check(lib().dd_iterate(self._h, k), "iterate", (OK,) if check else (OK, ENOCONV))
 
@@ -291,9 +296,9 @@ class DD:
         self._check(lib().dd_phase_profile(self._h, out.ctypes.data), "phase_profile")
         return out.reshape(2, 16)
 
-    def cell_stats(self, flags=False):
-        """Per composite cell of the last sweep: (iters, box_side, mufu_ops, kcycles[, flags]) arrays."""
-        n = lib().dd_get_cell_stats(self._h, None, None, None, None, None, 0)
+    def cell_stats(self, flags=False, err=False):
+        """Per composite cell of the last sweep: (iters, box_side, mufu_ops, kcycles[, flags][, err_x]) arrays."""
+        n = lib().dd_get_cell_stats(self._h, None, None, None, None, None, None, 0)
         if n < 0:
             raise RuntimeError(f"dd_get_cell_stats rc={-n}: {self.last_error()}")
         it = np.zeros(max(n, 1), np.int32)
@@ -301,11 +306,15 @@ class DD:
         mf = np.zeros(max(n, 1), np.float64)
         kc = np.zeros(max(n, 1), np.int32)
         fl = np.zeros(max(n, 1), np.int32)
+        ex = np.zeros(max(n, 1), np.float32)
         lib().dd_get_cell_stats(self._h, it.ctypes.data, bx.ctypes.data, mf.ctypes.data, kc.ctypes.data,
-                                fl.ctypes.data, n)
+                                fl.ctypes.data, ex.ctypes.data, n)
+        out = (it[:n], bx[:n], mf[:n], kc[:n])
         if flags:
-            return it[:n], bx[:n], mf[:n], kc[:n], fl[:n]
-        return it[:n], bx[:n], mf[:n], kc[:n]
+            out = out + (fl[:n],)
+        if err:
+            out = out + (ex[:n].astype(np.float64),)
+        return out
 
     def state_info(self):
         inf = StateInfo()

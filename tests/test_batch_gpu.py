@@ -62,3 +62,28 @@ def test_batch_argument_checks(mods):
     c = DD(mu2, nu2, 0.5 / 128**2, 4, schedule=1, coarsest_side=8)
     with pytest.raises(RuntimeError, match="differs"):
         run_batch([a, c])
+
+
+@pytest.mark.parametrize("n,s", [(256, 4), (128, 8)])
+def test_poisoned_memory_bit_identical(mods, n, s):
+    """No step of the path reads memory it did not write: with DD_POISON=1
+    every state / scratch buffer starts as 0xFF bytes (NaN) and K1 fills its
+    SMEM likewise; the final state must equal the clean run bit for bit (a
+    stale read would change a speculative-window decision or a value)."""
+    import os
+    DD, _ = mods
+    mu, nu = _imgs(n, 1)
+    eps = 0.5 / n**2
+    kw = dict(schedule=1, coarsest_side=8, max_inner_iter=100000, bcap_main=18 if s == 8 else 0)
+    ref = DD(mu, nu, eps, s, **kw)
+    ref.run_schedule()
+    a = ref.get_state()
+    os.environ["DD_POISON"] = "1"
+    try:
+        g = DD(mu, nu, eps, s, **kw)
+    finally:
+        del os.environ["DD_POISON"]
+    g.run_schedule()
+    b = g.get_state()
+    for key in ("boxes", "offsets", "values", "alpha_A", "alpha_B"):
+        assert np.array_equal(a[key], b[key]), key

@@ -23,7 +23,8 @@ ap.add_argument("--pair", type=int, default=0)
 ap.add_argument("--side", type=int, default=1024)
 ap.add_argument("--kappa", type=float, default=0.5)
 ap.add_argument("--sweep", type=int, default=1)
-ap.add_argument("--cells", default="3771")
+ap.add_argument("--cells", default="")
+ap.add_argument("--top", type=int, default=0, help="the top-K iteration cells of that sweep instead")
 ap.add_argument("--max-iter", type=int, default=100000)
 ap.add_argument("--gpu-max-iter", type=int, default=100000)
 a = ap.parse_args()
@@ -32,7 +33,6 @@ n, s = p["n"], p["s"]
 mu, nu = config_images(a.cfg, pair=a.pair)
 g = DD(mu, nu, p["kappa_final"] / n**2, s, schedule=SCHED_LADDER, coarsest_side=p.get("coarsest", 8),
        max_inner_iter=a.gpu_max_iter)
-cells = np.array([int(c) for c in a.cells.split(",")], np.int32)
 done = False
 for side, kappa, sweeps in build_schedule(n, p.get("coarsest", 8), p["kappa_final"]):
     while g.state_info()["side"] < side:
@@ -49,6 +49,10 @@ g.synchronize(check=False)
 before = g.get_state()
 g.iterate(1, check=False)
 it, bx, mf, kc, fl = g.cell_stats(flags=True)
+if a.top:
+    cells = np.argsort(-it)[:a.top].astype(np.int32)
+else:
+    cells = np.array([int(c) for c in a.cells.split(",")], np.int32)
 part = g.state_info()["last_partition"]
 print("gpu:", [(int(c), int(it[c]), int(bx[c]), int(fl[c])) for c in cells], flush=True)
 # the layer's images for the oracle: sum-pool the finest images to this side (A20)

@@ -660,6 +660,26 @@ int ddo_iterate(ddo_ctx* c, int n_half_iters) {
 }
 
 /* ------------------------------------------------------------ refinement -- */
+static int glue_alpha(ddo_ctx* c, double* ah);
+
+/* P:1508 "linear interpolation onto the fine points (in log space)": alpha
+ * = eps log u is the log-space potential; bilinear in coarse pixel-index
+ * coordinates at the fine pixel centres, (i + 1/2)/2 - 1/2, constant
+ * beyond the outermost coarse centres (reading A26). */
+static double interp_bilinear(const double* ph, int sc, int i, int j) {
+    double u = 0.5 * i - 0.25, v = 0.5 * j - 0.25;
+    if (u < 0.0) u = 0.0;
+    if (v < 0.0) v = 0.0;
+    if (u > sc - 1) u = sc - 1;
+    if (v > sc - 1) v = sc - 1;
+    int i0 = (int)u, j0 = (int)v;
+    int i1 = i0 + 1 < sc ? i0 + 1 : i0, j1 = j0 + 1 < sc ? j0 + 1 : j0;
+    double fu = u - i0, fv = v - j0;
+    double top = ph[(size_t)i0 * sc + j0] * (1.0 - fv) + ph[(size_t)i0 * sc + j1] * fv;
+    double bot = ph[(size_t)i1 * sc + j0] * (1.0 - fv) + ph[(size_t)i1 * sc + j1] * fv;
+    return top * (1.0 - fu) + bot * fu;
+}
+
 /* eq. FineBasicMarginals:
  *   nu_i^0(y) = nu(y) * nuhat_{Pa(i)}(pa(y)) / nuhat(pa(y)) * mu(X_i) / muhat(Xhat_{Pa(i)})
  * with 0/0 := 0.  Fine box = 2x the parent box.  alpha cold start (A14). */
@@ -669,6 +689,13 @@ int ddo_refine(ddo_ctx* c) {
     layer_t* Lc = &c->L[c->cur];
     layer_t* Lf = &c->L[c->cur + 1];
     int nbc = Lc->nb, nbf = Lf->nb;
+    double* ah = NULL;                  /* glued coarse potentials (warm_refine) */
+    if (c->opt.warm_refine && c->last_part != 0) {
+        ah = (double*)malloc((size_t)Lc->side * Lc->side * sizeof(double));
+        if (!ah) return DDO_ENOMEM;
+        int rc = glue_alpha(c, ah);
+        if (rc) { free(ah); return rc; }
+    }
     int* nbox = (int*)calloc((size_t)nbf * nbf * 4, sizeof(int));
     double** nval = (double**)calloc((size_t)nbf * nbf, sizeof(double*));
     if (!nbox || !nval) return DDO_ENOMEM;
@@ -702,7 +729,16 @@ int ddo_refine(ddo_ctx* c) {
     size_t n2 = (size_t)Lf->side * Lf->side;
     c->alphaA = (double*)calloc(n2, sizeof(double));
     c->alphaB = (double*)calloc(n2, sizeof(double));
-    if (!c->alphaA || !c->alphaB) return DDO_ENOMEM;
+    if (!c->alphaA || !c->alphaB) { free(ah); return DDO_ENOMEM; }
+    if (ah) {                           /* both partitions start from the same alpha */
+        for (int i = 0; i < Lf->side; ++i)
+            for (int j = 0; j < Lf->side; ++j) {
+                double a = interp_bilinear(ah, Lc->side, i, j);
+                c->alphaA[(size_t)i * Lf->side + j] = a;
+                c->alphaB[(size_t)i * Lf->side + j] = a;
+            }
+        free(ah);
+    }
     c->last_part = 0;
     return DDO_OK;
 }
@@ -850,24 +886,24 @@ static void glue_matvec(int nb, const double* x, double* y) {
         }
 }
 
-int ddo_dual_gap(ddo_ctx* c, double* primal, double* dual, double* rel) {
-    if (!c) return DDO_EINVAL;
+/* Sec. 6.3: glue the partitions' cell potentials into one
+ * dual candidate on the current layer: per basic cell i the mu-weighted
+ * averages a_i = log avg exp((alpha_A - alpha_B)/eps), b_i = log avg
+ * exp((alpha_B - alpha_A)/eps) give the edge weights of the A-cell graph;
+ * V = the least-squares solution of V(J2) - V(J1) = log q (reading A25),
+ * zero mean; ah = alpha_A + eps V(A(x)).  Plain CG (the Laplacian is
+ * singular only in the constants; R has zero sum). */
+static int glue_alpha(ddo_ctx* c, double* ah) {
     layer_t* L = &c->L[c->cur];
     int side = L->side, s = L->s, nb = L->nb, na = nb / 2;
     double eps = c->eps;
-    double ent = 0;
-    int rc = evaluate(c, NULL, &ent, NULL);
-    if (rc) return rc;
-    double P = ent / eps;                                  /* KL(pi|K) - ||K|| */
-    /* a_i = log avg_{X_i} exp((aA - aB)/eps) dmu, b_i = log avg exp((aB - aA)/eps) dmu */
     int nbb = nb * nb;
     double* ab = (double*)calloc((size_t)2 * nbb, sizeof(double));
     int n = na * na;
     double* V = (double*)calloc((size_t)(n > 0 ? n : 1) * 4, sizeof(double));
     size_t n2 = (size_t)side * side;
-    double* ah = (double*)malloc(n2 * sizeof(double));
-    double* T = (double*)malloc(n2 * sizeof(double));
-    if (!ab || !V || !ah || !T) { free(ab); free(V); free(ah); free(T); return DDO_ENOMEM; }
+    if (!ab || !V) { free(ab); free(V); return DDO_ENOMEM; }
+    /* a_i = log avg_{X_i} exp((aA - aB)/eps) dmu, b_i = log avg exp((aB - aA)/eps) dmu */
     for (int i = 0; i < nbb; ++i) {
         int r0 = (i / nb) * s, c0 = (i % nb) * s;
         double mp = -INFINITY, mn = -INFINITY, sm = 0;
@@ -932,6 +968,25 @@ int ddo_dual_gap(ddo_ctx* c, double* primal, double* dual, double* rel) {
         int r = (int)(g / side), q = (int)(g % side);
         ah[g] = c->alphaA[g] + eps * V[(r / s / 2) * na + (q / s / 2)];
     }
+    free(ab); free(V);
+    return DDO_OK;
+}
+
+int ddo_dual_gap(ddo_ctx* c, double* primal, double* dual, double* rel) {
+    if (!c) return DDO_EINVAL;
+    layer_t* L = &c->L[c->cur];
+    int side = L->side;
+    double eps = c->eps;
+    double ent = 0;
+    int rc = evaluate(c, NULL, &ent, NULL);
+    if (rc) return rc;
+    double P = ent / eps;                                  /* KL(pi|K) - ||K|| */
+    size_t n2 = (size_t)side * side;
+    double* ah = (double*)malloc(n2 * sizeof(double));
+    double* T = (double*)malloc(n2 * sizeof(double));
+    if (!ah || !T) { free(ah); free(T); return DDO_ENOMEM; }
+    rc = glue_alpha(c, ah);
+    if (rc) { free(ah); free(T); return rc; }
     /* Y-iteration against u_hat, dense (log v_hat below) */
     ksum_t dsum = {0, 0};
     for (size_t g = 0; g < n2; ++g)
@@ -966,7 +1021,7 @@ int ddo_dual_gap(ddo_ctx* c, double* primal, double* dual, double* rel) {
     if (primal) *primal = P;
     if (dual) *dual = D;
     if (rel) *rel = (P - D) / P;
-    free(ab); free(V); free(ah); free(T);
+    free(ah); free(T);
     return DDO_OK;
 }
 

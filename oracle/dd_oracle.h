@@ -42,6 +42,10 @@ typedef struct {
     int no_truncate;       /* 1 -> tau = 0 exactly (pins P3/P5) */
     int empty_init;        /* 1 -> no product initialisation: empty state, a state is imported next */
     int check_every;       /* stop-test cadence k (reading A5): stop at it % k == 0; 0 -> 1 */
+    int warm_refine;       /* 1 -> ddo_refine warm-starts alpha as P:1507-1508 does: the
+                              coarse potentials glued (Sec. 6.3) and
+                              interpolated linearly in log space onto the fine pixel
+                              centres (readings A25, A26); 0 -> cold start alpha = 0 (A14) */
 } ddo_options;
 
 typedef struct {

@@ -325,3 +325,46 @@ def test_pool_overflow_reports_enomem(DD):
     g = DD(mu, nu, 0.5 / 64**2, 4, schedule=1, coarsest_side=16, pool_capacity=16 * 16 * 16 * 16 + 64)
     with pytest.raises(RuntimeError, match="rc=6"):
         g.run_schedule()
+
+
+def test_warm_refine_k5_vs_oracle(DD):
+    """K5 (glue + log-space interpolation) vs the oracle's
+    warm_refine on the same imported coarse state: the fine potentials of
+    both partitions agree (fp64 on both sides; CG tolerances)."""
+    from oracle.oracle import SCHED_LADDER as OL
+    mu, nu = config_images(2)
+    n = 64
+    o = Oracle(mu, nu, 0.5 / n**2, 4, schedule=OL, coarsest_side=32, warm_refine=True)
+    o.set_eps(1.0 / 32**2)
+    o.iterate(6)
+    st = o.get_state()
+    g = DD(mu, nu, 0.5 / n**2, 4, schedule=1, coarsest_side=32)
+    g.set_eps(1.0 / 32**2)
+    g.set_state(st)
+    g.refine()
+    o.refine()
+    a, b = g.get_state(), o.get_state()
+    scale = np.abs(b["alpha_A"]).max()
+    for key in ("alpha_A", "alpha_B"):
+        d = a[key] - b[key]
+        d -= d.mean()                     # the glued potential's global constant is a gauge (P:222)
+        assert np.abs(d).max() <= 1e-9 * max(scale, 1e-12), (key, np.abs(d).max(), scale)
+
+
+def test_ladder_parity_both_warm_cfg2(DD):
+    """cfg-2 ladder with the paper's warm start on BOTH sides (GPU K5 default,
+    oracle warm_refine): the BASELINE gates."""
+    from oracle.oracle import SCHED_LADDER as OL
+    mu, nu = config_images(2)
+    n = 64
+    g = DD(mu, nu, 0.5 / n**2, 4, schedule=1, coarsest_side=16, eps_start=1.0)
+    o = Oracle(mu, nu, 0.5 / n**2, 4, schedule=OL, coarsest_side=16, eps_start=1.0, warm_refine=True)
+    g.run_schedule()
+    o.run_schedule()
+    cg, _ = g.primal_cost()
+    co, _ = o.primal_cost()
+    assert abs(cg - co) <= 1e-5 * co, (cg, co)
+    lx, ly = g.marginal_error()
+    assert lx <= 1e-6 and ly <= 1e-6
+    Dg, Do = g.basic_marginals_dense(), o.basic_marginals_dense()
+    assert np.abs(Dg - Do).sum() <= 4e-6     # sum_J 2 Err ||mu_J|| (P9, different stop iterations)

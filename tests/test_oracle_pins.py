@@ -456,3 +456,76 @@ def test_marginal_error_l1y_pin(dm, ds):
     if dm == 0.0 or ds == 0.0:
         assert abs(want - (2 * dm + ds)) <= 1e-15
     assert abs(ly - want) <= 1e-13 + 1e-10 * want, (ly, want)
+
+
+# ----------------------------------------------- f1: warm-start refinement --
+def _bilinear_a26(ph, i, j):
+    """Reading A26 written out: fine centre (i + 1/2)/2 - 1/2 in coarse index
+    units, bilinear, constant beyond the outermost coarse centres."""
+    sc = ph.shape[0]
+    u = min(max(0.5 * i - 0.25, 0.0), sc - 1.0)
+    v = min(max(0.5 * j - 0.25, 0.0), sc - 1.0)
+    i0, j0 = int(u), int(v)
+    i1, j1 = min(i0 + 1, sc - 1), min(j0 + 1, sc - 1)
+    fu, fv = u - i0, v - j0
+    return ((1 - fu) * ((1 - fv) * ph[i0, j0] + fv * ph[i0, j1]) + fu * ((1 - fv) * ph[i1, j0] + fv * ph[i1, j1]))
+
+
+def test_warm_refine_glues_and_interpolates():
+    """P:1507-1508 (f1): alpha_A = phi + k_A(J_A(x)), alpha_B = phi + k_B(J_B(x))
+    with arbitrary per-cell constants (the gauge freedom of each cell's
+    potential): gluing (Sec. 6.3, reading A25) must recover phi up to
+    one global constant, and the fine potentials of BOTH partitions are its
+    log-space linear interpolation (reading A26)."""
+    from oracle.oracle import SCHED_LADDER
+    n, s = 32, 4
+    mu, nu = config_images(1)
+    o = Oracle(mu, nu, 2.0 / 16**2, s, schedule=SCHED_LADDER, coarsest_side=16, warm_refine=True)
+    st = o.get_state()
+    side, nb = st["info"]["side"], st["info"]["nb"]
+    assert side == 16
+    rng = np.random.default_rng(7)
+    ii, jj = np.meshgrid(np.arange(side), np.arange(side), indexing="ij")
+    phi = 1e-3 * (np.sin(ii / 3.0) + 0.5 * np.cos(jj / 5.0) + 0.01 * ii * jj)
+    na, nbB = nb // 2, nb // 2 + 1
+    kA = rng.normal(size=(na, na)) * 1e-2
+    kB = rng.normal(size=(nbB, nbB)) * 1e-2
+    cellA = (ii // s) // 2, (jj // s) // 2
+    cellB = (ii // s + 1) // 2, (jj // s + 1) // 2
+    st["alpha_A"] = phi + kA[cellA]
+    st["alpha_B"] = phi + kB[cellB]
+    st["info"]["last_partition"] = 2
+    o.set_state(st)
+    o.refine()
+    fine = o.get_state()
+    aA, aB = fine["alpha_A"], fine["alpha_B"]
+    assert aA.shape == (32, 32)
+    np.testing.assert_array_equal(aA, aB)
+    ref = np.array([[_bilinear_a26(phi, i, j) for j in range(32)] for i in range(32)])
+    d = aA - ref
+    assert np.ptp(d) < 1e-12, np.ptp(d)
+
+
+def test_warm_refine_ladder_faster_same_answer():
+    """The warm start only changes the Sinkhorn iteration counts (the cell
+    optimum is unique): same cost to 1e-6 relative, fewer iterations."""
+    from oracle.oracle import SCHED_LADDER, build_schedule
+    mu, nu = config_images(2)
+    res = {}
+    for warm in (False, True):
+        o = Oracle(mu, nu, 0.5 / 64**2, 4, schedule=SCHED_LADDER, coarsest_side=16, eps_start=1.0,
+                   warm_refine=warm)
+        its, side = 0, 16
+        for sd, kappa, sweeps in build_schedule(64, 16, 0.5, 1.0):
+            while side < sd:
+                o.refine()
+                side *= 2
+            o.set_eps(kappa / sd**2)
+            for _ in range(sweeps):
+                o.iterate(1)
+                its += o.stats()["iters_sum"]
+        res[warm] = (o.primal_cost()[0], its, o.marginal_error())
+    (c0, i0, m0), (c1, i1, m1) = res[False], res[True]
+    assert abs(c1 - c0) <= 1e-6 * c0, (c0, c1)
+    assert m1[0] <= 1e-6 and m1[1] <= 1e-6
+    assert i1 < i0, (i0, i1)

@@ -254,6 +254,25 @@ int dd_export_rows(dd_ctx* ctx, int row, int nrows, void* buf, size_t* bytes);
  * halo region (one boundary row at a time; DD_ENOMEM if it does not fit). */
 int dd_import_rows(dd_ctx* ctx, int row, int nrows, const void* buf, size_t bytes);
 
+/* dd_compact -- K2 over the current pool: every stored box (including rows
+ * imported into the halo region) moves into the main pool in basic-cell
+ * order, freeing the halo slots (the multi-GPU driver calls it after moving
+ * rows between stripes).  Asynchronous. */
+int dd_compact(dd_ctx* ctx);
+
+/* dd_export_rows_slab / dd_import_rows_slab -- the same rows through a
+ * fixed-capacity DEVICE slab with no host-visible size, fully asynchronous
+ * on the context stream (the multi-GPU exchange sends the whole slab with a
+ * fixed NCCL count; no host synchronisation per exchange):
+ *   int64 header[8] {magic, n boxes, padded entries, bytes needed, overflow}
+ *   | int4 boxes[nrows*nb] | fp64 values (row-major, each padded to even).
+ * A slab too small for the rows (header: overflow = 1) or one that fails
+ * validation on import leaves the imported rows empty and is reported as
+ * DD_ENOMEM by the next dd_synchronize.  slab_bytes >= 64 + 16*nrows*nb + 16;
+ * size it from dd_export_rows(buf = NULL) once per layer.  Caller owns slab. */
+int dd_export_rows_slab(dd_ctx* ctx, int row, int nrows, void* slab, size_t slab_bytes);
+int dd_import_rows_slab(dd_ctx* ctx, int row, int nrows, const void* slab, size_t slab_bytes);
+
 /* dd_copy_alpha -- copy pixel rows [row0, row0+nrows) of the X-potential
  * image alpha_A (partition 1) or alpha_B (2) of the current layer (fp64,
  * cost units, row-major, side columns) to (to_ctx = 0) or from (to_ctx = 1)

@@ -43,6 +43,11 @@ cudaError_t launch_k0_cluster(const int* sorted, int* counts, int ncap, const in
                               int mode, int* list3, cudaStream_t st);
 cudaError_t launch_k0(const SweepParams& p, int b0, int b1, int* lists, int* counts, int ncap, int* bside,
                       int* sorted, cudaStream_t st);
+cudaError_t launch_slab_export(const int4* box, const long long* off, const double* pool, int n, void* slab,
+                               long long cap_bytes, long long* scratch, int* flag, cudaStream_t st);
+cudaError_t launch_slab_import(const void* slab, int n, int side, long long hbase, long long slot, int4* box,
+                               long long* off, double* pool, long long pool_cap, long long* scratch, int* flag,
+                               cudaStream_t st);
 cudaError_t launch_pool2x2(const double* fine, double* coarse, int sc, cudaStream_t st);
 cudaError_t launch_log(const double* x, double* lx, long long n, cudaStream_t st);
 cudaError_t launch_mass_i(const double* mu, double* mass, int side, int s, int nb, cudaStream_t st);

@@ -224,6 +224,11 @@ int check_overflow(dd_ctx* c) {
         set_err(c, "a composite cell's Y box exceeds the largest supported box side (%d)", c->bcap_big2);
         return DD_ENOMEM;
     }
+    if (ov & 4) {
+        set_err(c, "a row slab overflowed its capacity or failed validation (dd_export_rows_slab / "
+                   "dd_import_rows_slab); the imported rows were left empty");
+        return DD_ENOMEM;
+    }
     return DD_OK;
 }
 
@@ -1101,6 +1106,51 @@ int dd_import_rows(dd_ctx* c, int row, int nrows, const void* buf, size_t bytes)
     CK(cudaMemcpyAsync(c->off + (size_t)row * Lr.nb, c->d_xoff + n, n * sizeof(long long), cudaMemcpyDeviceToDevice,
                        c->st));
     CK(cudaStreamSynchronize(c->st));
+    return DD_OK;
+}
+
+int dd_compact(dd_ctx* c) {
+    if (!c) return DD_EINVAL;
+    CK(cudaSetDevice(c->device));
+    const Layer& Lr = c->L[c->cur];
+    const int nb2 = Lr.nb * Lr.nb;
+    // K2 over the current pool: new basic-cell-order offsets, pool -> scratch, swap
+    CK(launch_scan_areas(c->box, c->off2, c->d_total, nb2, c->d_total + 1, c->st));
+    CK(launch_copy_boxes(c->box, c->off, c->off2, c->pool, c->scratch, nb2, c->cap - c->halo_cap, c->st));
+    std::swap(c->off, c->off2);
+    std::swap(c->pool, c->scratch);
+    return DD_OK;
+}
+
+int dd_export_rows_slab(dd_ctx* c, int row, int nrows, void* slab, size_t slab_bytes) {
+    if (!c || !slab) return DD_EINVAL;
+    CK(cudaSetDevice(c->device));
+    const Layer& Lr = c->L[c->cur];
+    if (row < 0 || nrows <= 0 || row + nrows > Lr.nb) { set_err(c, "rows out of range"); return DD_EINVAL; }
+    const int n = nrows * Lr.nb;
+    if (slab_bytes < (size_t)(64 + 16LL * n + 16)) { set_err(c, "slab smaller than its header"); return DD_EINVAL; }
+    int rc = ensure_xoff(c, 2LL * n);
+    if (rc) return rc;
+    CK(launch_slab_export(c->box + (size_t)row * Lr.nb, c->off + (size_t)row * Lr.nb, c->pool, n, slab,
+                          (long long)slab_bytes, c->d_xoff, c->counters + 6, c->st));
+    return DD_OK;
+}
+
+int dd_import_rows_slab(dd_ctx* c, int row, int nrows, const void* slab, size_t slab_bytes) {
+    if (!c || !slab) return DD_EINVAL;
+    CK(cudaSetDevice(c->device));
+    const Layer& Lr = c->L[c->cur];
+    if (row < 0 || nrows <= 0 || row + nrows > Lr.nb) { set_err(c, "rows out of range"); return DD_EINVAL; }
+    const int n = nrows * Lr.nb;
+    if (slab_bytes < (size_t)(64 + 16LL * n + 16)) { set_err(c, "slab smaller than its header"); return DD_EINVAL; }
+    int rc = ensure_xoff(c, 2LL * n);
+    if (rc) return rc;
+    // the same two halo slots as dd_import_rows (rows above the stripe | the
+    // stripe's own rows returned by the rank below)
+    const long long slot = c->halo_cap / 2;
+    const long long hbase = c->cap - c->halo_cap + ((row < c->stripe_lo) ? 0 : slot);
+    CK(launch_slab_import(slab, n, Lr.side, hbase, slot, c->box + (size_t)row * Lr.nb, c->off + (size_t)row * Lr.nb,
+                          c->pool, c->cap, c->d_xoff, c->counters + 6, c->st));
     return DD_OK;
 }
 

@@ -108,6 +108,83 @@ __global__ void k_copy_boxes(const int4* __restrict__ box, const long long* __re
     if ((a & 1) && l == 0) dst[d0 + a - 1] = src[so + a - 1];
 }
 
+// ------------------------------------------------ multi-GPU row slabs --
+// A fixed-capacity slab carries basic-cell rows between stripes with no
+// host-visible size:
+//   int64 hdr[8] = {magic, n boxes, padded entries, bytes needed, overflow}
+//   int4 boxes[n] | fp64 values (each box row-major, padded to even length)
+// Pack: exclusive scan of the padded areas (one block), header, boxes, and
+// the per-box slab offsets for k_copy_boxes (which skips boxes past cap).
+constexpr long long kSlabMagic = 0x44445342414c53LL;
+__host__ __device__ inline long long slab_values_off(int n) { return (64 + 16LL * n + 15) & ~15LL; }
+
+__global__ void k_slab_pack(const int4* __restrict__ box, int n, long long cap_bytes, long long* __restrict__ hdr,
+                            int4* __restrict__ sbox, long long* __restrict__ dstoff, int* __restrict__ flag) {
+    __shared__ long long part[1024];
+    const int t = threadIdx.x;
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int b = t * per, e = min(n, b + per);
+    long long s = 0;
+    for (int k = b; k < e; ++k) s += ((long long)box[k].z * box[k].w + 1) & ~1LL;
+    part[t] = s;
+    __syncthreads();
+    if (t == 0) {
+        long long acc = 0;
+        for (int k = 0; k < (int)blockDim.x; ++k) { const long long v = part[k]; part[k] = acc; acc += v; }
+        const long long need = slab_values_off(n) + 8 * acc;
+        const long long ov = need > cap_bytes ? 1 : 0;
+        hdr[0] = kSlabMagic; hdr[1] = n; hdr[2] = acc; hdr[3] = need; hdr[4] = ov;
+        if (ov) atomicOr(flag, 4);
+    }
+    __syncthreads();
+    long long o = part[t];
+    for (int k = b; k < e; ++k) {
+        sbox[k] = box[k];
+        dstoff[k] = o;
+        o += ((long long)box[k].z * box[k].w + 1) & ~1LL;
+    }
+}
+
+// Unpack: validate the slab (magic, box count, bounds, overflow), then the
+// boxes go to the context's arrays and their values to the halo slot at
+// hbase (offsets by an exclusive scan); invalid -> empty boxes + flag 4.
+__global__ void k_slab_unpack(const long long* __restrict__ hdr, const int4* __restrict__ sbox, int n, int side,
+                              long long hbase, long long slot, int4* __restrict__ box, long long* __restrict__ off,
+                              long long* __restrict__ srcoff, long long* __restrict__ dstoff, int* __restrict__ flag) {
+    __shared__ long long part[1024];
+    __shared__ int bad;
+    const int t = threadIdx.x;
+    if (t == 0) bad = (hdr[0] != kSlabMagic || hdr[1] != n || hdr[4] != 0) ? 1 : 0;
+    __syncthreads();
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int b = t * per, e = min(n, b + per);
+    long long s = 0;
+    for (int k = b; k < e; ++k) {
+        const int4 q = sbox[k];
+        if (q.x < 0 || q.y < 0 || q.z < 0 || q.w < 0 || q.x + q.z > side || q.y + q.w > side) bad = 1;
+        s += ((long long)q.z * q.w + 1) & ~1LL;
+    }
+    part[t] = s;
+    __syncthreads();
+    if (t == 0) {
+        long long acc = 0;
+        for (int k = 0; k < (int)blockDim.x; ++k) { const long long v = part[k]; part[k] = acc; acc += v; }
+        if (acc > slot || (!bad && acc != hdr[2])) bad = 1;
+        if (bad) atomicOr(flag, 4);
+    }
+    __syncthreads();
+    long long o = part[t];
+    for (int k = b; k < e; ++k) {
+        const int4 q = sbox[k];
+        const long long a = ((long long)q.z * q.w + 1) & ~1LL;
+        box[k] = bad ? make_int4(0, 0, 0, 0) : q;
+        off[k] = bad ? 0 : hbase + o;
+        srcoff[k] = o;
+        dstoff[k] = hbase + o;
+        o += a;
+    }
+}
+
 // ------------------------------------------------------------------- K3 --
 // Fixed-order reduction of the per-cell outputs into the sweep statistics
 // (one block of 1024 threads; thread t owns cells t, t+1024, ... in order).
@@ -432,6 +509,31 @@ cudaError_t launch_copy_boxes(const int4* box, const long long* srcoff, const lo
                               double* dst, int n, long long cap, cudaStream_t st) {
     const int wpb = 8;
     k_copy_boxes<<<(n + wpb - 1) / wpb, 32 * wpb, 0, st>>>(box, srcoff, dstoff, src, dst, n, cap);
+    LAUNCH_CHECK(); return cudaSuccess;
+}
+cudaError_t launch_slab_export(const int4* box, const long long* off, const double* pool, int n, void* slab,
+                               long long cap_bytes, long long* scratch, int* flag, cudaStream_t st) {
+    char* b = (char*)slab;
+    long long* hdr = (long long*)b;
+    int4* sbox = (int4*)(b + 64);
+    const long long vo = slab_values_off(n);
+    k_slab_pack<<<1, 1024, 0, st>>>(box, n, cap_bytes, hdr, sbox, scratch, flag);
+    LAUNCH_CHECK();
+    const long long vcap = cap_bytes > vo ? (cap_bytes - vo) / 8 : 0;
+    const int wpb = 8;
+    k_copy_boxes<<<(n + wpb - 1) / wpb, 32 * wpb, 0, st>>>(box, off, scratch, pool, (double*)(b + vo), n, vcap);
+    LAUNCH_CHECK(); return cudaSuccess;
+}
+cudaError_t launch_slab_import(const void* slab, int n, int side, long long hbase, long long slot, int4* box,
+                               long long* off, double* pool, long long pool_cap, long long* scratch, int* flag,
+                               cudaStream_t st) {
+    const char* b = (const char*)slab;
+    k_slab_unpack<<<1, 1024, 0, st>>>((const long long*)b, (const int4*)(b + 64), n, side, hbase, slot, box, off,
+                                      scratch, scratch + n, flag);
+    LAUNCH_CHECK();
+    const int wpb = 8;
+    k_copy_boxes<<<(n + wpb - 1) / wpb, 32 * wpb, 0, st>>>(box, scratch, scratch + n,
+                                                          (const double*)(b + slab_values_off(n)), pool, n, pool_cap);
     LAUNCH_CHECK(); return cudaSuccess;
 }
 cudaError_t launch_reduce_stats(const CellOut* out, int ncells, DevStats* last, DevStats* tot,

@@ -24,7 +24,7 @@ PLAN_BASIC_MARGINALS, PLAN_COO = 0, 1
 EXPORTS = ["dd_init", "dd_iterate", "dd_set_eps", "dd_set_max_inner_iter", "dd_refine", "dd_run_schedule", "dd_run_schedule_batch", "dd_reset",
            "dd_primal_cost", "dd_dual_gap", "dd_marginal_error", "dd_fetch_plan", "dd_get_stats", "dd_get_totals",
            "dd_reset_totals", "dd_set_stripe", "dd_clear_rows", "dd_export_rows",
-           "dd_import_rows", "dd_copy_alpha", "dd_y_accumulate", "dd_y_l1", "dd_phase_profile", "dd_get_cell_stats", "dd_get_state_info", "dd_get_state", "dd_set_state",
+           "dd_import_rows", "dd_export_rows_slab", "dd_import_rows_slab", "dd_compact", "dd_copy_alpha", "dd_y_accumulate", "dd_y_l1", "dd_phase_profile", "dd_get_cell_stats", "dd_get_state_info", "dd_get_state", "dd_set_state",
            "dd_build_schedule", "dd_measure_mufu_peak", "dd_synchronize", "dd_free",
            "dd_last_error", "dd_version"]
 
@@ -90,6 +90,11 @@ def lib():
         L.dd_clear_rows.argtypes = [p, i, i]
         L.dd_export_rows.argtypes = [p, i, i, p, C.POINTER(C.c_size_t)]
         L.dd_import_rows.argtypes = [p, i, i, p, C.c_size_t]
+        if hasattr(L, "dd_compact"):
+            L.dd_compact.argtypes = [p]
+        if hasattr(L, "dd_export_rows_slab"):
+            L.dd_export_rows_slab.argtypes = [p, i, i, p, C.c_size_t]
+            L.dd_import_rows_slab.argtypes = [p, i, i, p, C.c_size_t]
         L.dd_y_accumulate.argtypes = [p, p]
         L.dd_copy_alpha.argtypes = [p, i, i, i, p, i]
         L.dd_y_l1.argtypes = [p, p, C.POINTER(d)]
@@ -277,6 +282,18 @@ class DD:
     def import_rows(self, row, nrows, dev_buf, nbytes):
         return self._check(lib().dd_import_rows(self._h, row, nrows, C.c_void_p(dev_buf.data_ptr()), nbytes),
                            "import_rows")
+
+    def compact(self):
+        return self._check(lib().dd_compact(self._h), "compact")
+
+    def export_rows_slab(self, row, nrows, slab):
+        """Asynchronous export into a fixed-capacity device slab (uint8 tensor)."""
+        return self._check(lib().dd_export_rows_slab(self._h, row, nrows, C.c_void_p(slab.data_ptr()),
+                                                     slab.numel() * slab.element_size()), "export_rows_slab")
+
+    def import_rows_slab(self, row, nrows, slab):
+        return self._check(lib().dd_import_rows_slab(self._h, row, nrows, C.c_void_p(slab.data_ptr()),
+                                                     slab.numel() * slab.element_size()), "import_rows_slab")
 
     def copy_alpha(self, partition, row0, nrows, dev_buf, to_ctx):
         return self._check(lib().dd_copy_alpha(self._h, partition, row0, nrows, C.c_void_p(dev_buf.data_ptr()),

@@ -37,6 +37,33 @@ def stripe_bounds(nb: int, nranks: int):
     return b
 
 
+def balanced_bounds(nb: int, row_work, nranks: int, old=None):
+    """Cost-aware even bounds: split the per-A-cell-row predicted work
+    (row_work[q], q < nb/2) into nranks contiguous runs of nearly equal
+    work (greedy on the prefix sums).  With `old` bounds, each new bound
+    stays strictly between its old neighbours, so a basic row moves at most
+    one rank per rebalance."""
+    half = nb // 2
+    w = np.asarray(row_work, dtype=np.float64)
+    c = np.concatenate([[0.0], np.cumsum(w)])
+    tot = c[-1]
+    if not tot > 0:
+        return stripe_bounds(nb, nranks)
+    b = [0]
+    for r in range(1, nranks):
+        q = int(np.searchsorted(c, tot * r / nranks))
+        if q > 0 and abs(c[q - 1] - tot * r / nranks) < abs(c[q] - tot * r / nranks):
+            q -= 1
+        lo_q = b[-1] // 2 + 1
+        hi_q = half - (nranks - r)
+        if old is not None:
+            lo_q = max(lo_q, old[r - 1] // 2 + 1)
+            hi_q = min(hi_q, old[r + 1] // 2 - 1)
+        b.append(2 * min(max(q, lo_q), max(lo_q, hi_q)))
+    b.append(nb)
+    return b
+
+
 def owned_cell_rows(nb: int, part: int, lo: int, hi: int):
     """Partition cell rows [q0, q1) solved by the stripe [lo, hi) (engine.cu cell_rows)."""
     q0 = lo // 2
@@ -60,6 +87,14 @@ class LocalTransport:
 
     def exchange(self, sends, expects):
         """sends: [(src, dst, tensor)]; expects: [(src, dst)] -> {(src, dst): tensor}."""
+        got = {(s, d): t for s, d, t in sends}
+        return {k: got[k] for k in expects}
+
+    def exchange_fixed(self, sends, expects, recv_bufs):
+        """Fixed-size slabs: the receiver reads the sender's slab (contexts on
+        different streams of one device: order them by a device sync)."""
+        import torch
+        torch.cuda.synchronize()
         got = {(s, d): t for s, d, t in sends}
         return {k: got[k] for k in expects}
 
@@ -113,6 +148,26 @@ class TorchTransport:
                 w.wait()
         return out
 
+    def exchange_fixed(self, sends, expects, recv_bufs):
+        """One round of fixed-size slabs (NCCL needs matching counts; the
+        slab's header carries the real size): no size round, no .item().
+        work.wait() orders the current stream after the NCCL ops on the
+        device -- no host synchronisation."""
+        if self.staging:
+            cpu = TorchTransport(self.dist, self.rank, self.nranks, self.staging)
+            rb = {k: v.to(self.staging) for k, v in recv_bufs.items()}
+            got = cpu.exchange_fixed([(s, d, t.to(self.staging)) for s, d, t in sends], expects, rb)
+            for k, v in got.items():
+                recv_bufs[k].copy_(v)
+            return recv_bufs
+        d = self.dist
+        ops = [d.P2POp(d.isend, t, dst) for s, dst, t in sends]
+        ops += [d.P2POp(d.irecv, recv_bufs[k], k[0]) for k in expects]
+        if ops:
+            for w in d.batch_isend_irecv(ops):
+                w.wait()
+        return {k: recv_bufs[k] for k in expects}
+
     def _reduce(self, t, op):
         if self.staging:
             h = t.to(self.staging)
@@ -137,7 +192,8 @@ class StripedRun:
     torch.distributed, all ranks for LocalTransport); every DD must be in
     DD_SCHED_LADDER or FIXED mode on the same inputs."""
 
-    def __init__(self, ranks, nranks: int, transport, device="cuda"):
+    def __init__(self, ranks, nranks: int, transport, device="cuda", slab_factor: float = 2.0,
+                 cost_aware: bool = True):
         self.ranks = list(ranks)
         self.nranks = nranks
         self.tr = transport
@@ -147,6 +203,12 @@ class StripedRun:
         self.nb = None
         self.exchanged_bytes = 0
         self.cells_solved = 0
+        self.slab_factor = slab_factor
+        self.cost_aware = cost_aware
+        self.a_work = None               # per A-cell row work of the last recorded A-sweep
+        self.rebalances = 0
+        self.slab_bytes = 0
+        self.slabs = {}                  # (rank, "send"|"recv") -> uint8 device tensor
 
     # -- layer setup
     def _layer(self, prev=None):
@@ -165,6 +227,32 @@ class StripedRun:
                 dd.set_stripe(0, 0)
             else:
                 dd.set_stripe(self.bounds[r], self.bounds[r + 1])
+        if self.bounds is not None:
+            self._size_slabs()
+
+    def _size_slabs(self):
+        """Once per layer (the layer change synchronises anyway): the slab
+        capacity = slab_factor x the largest boundary-row payload of the
+        refined state, the same on every rank (max all-reduce); rounded up
+        to 1 MiB.  An exchange that outgrows it is reported by the library
+        (DD_ENOMEM at the next dd_synchronize), never truncated silently."""
+        import torch
+        b, N = self.bounds, self.nranks
+        need = 0
+        for r, dd in self.ranks:
+            rows = ([b[r + 1] - 1] if r < N - 1 else []) + ([b[r] - 1] if r > 0 else [])
+            for row in rows:
+                need = max(need, dd.export_rows_size(row, 1))
+        t = self.tr.allreduce_max(torch.tensor([float(need)], dtype=torch.float64, device=self.device))
+        need = int(t.item())
+        cap = int(need * self.slab_factor) + (1 << 16)
+        cap = ((cap + (1 << 20) - 1) >> 20) << 20
+        if cap != self.slab_bytes:
+            self.slab_bytes = cap
+            self.slabs = {}
+            for r, _ in self.ranks:
+                for kind in ("send", "recv_lo", "recv_hi"):
+                    self.slabs[(r, kind)] = torch.empty(cap, dtype=torch.uint8, device=self.device)
 
     def start(self):
         """Call after init / reset (coarsest layer) or after a refine."""
@@ -220,32 +308,37 @@ class StripedRun:
 
     def _pass_rows(self, down: bool):
         """down: row hi-1 of rank p -> rank p+1 (before a B-sweep);
-        up: row lo-1 of rank p -> rank p-1 (after it)."""
+        up: row lo-1 of rank p -> rank p-1 (after it).  Fixed-capacity slabs,
+        packed and unpacked on the device (dd_export_rows_slab /
+        dd_import_rows_slab), one send/recv round: no host synchronisation."""
         b, N = self.bounds, self.nranks
-        sends, expects = [], []
+        sends, expects, recv = [], [], {}
         for r, dd in self.ranks:
             if down and r < N - 1:
                 row = b[r + 1] - 1
-                sends.append((r, r + 1, self._export(dd, row)))
+                dd.export_rows_slab(row, 1, self.slabs[(r, "send")])
                 dd.clear_rows(row, 1)
+                sends.append((r, r + 1, self.slabs[(r, "send")]))
             if not down and r > 0:
                 row = b[r] - 1
-                sends.append((r, r - 1, self._export(dd, row)))
+                dd.export_rows_slab(row, 1, self.slabs[(r, "send")])
                 dd.clear_rows(row, 1)
+                sends.append((r, r - 1, self.slabs[(r, "send")]))
             if down and r > 0:
                 expects.append((r - 1, r))
+                recv[(r - 1, r)] = self.slabs[(r, "recv_lo")]
             if not down and r < N - 1:
                 expects.append((r + 1, r))
-        got = self.tr.exchange(sends, expects)
+                recv[(r + 1, r)] = self.slabs[(r, "recv_hi")]
+        self.exchanged_bytes += self.slab_bytes * len(sends)
+        got = self.tr.exchange_fixed(sends, expects, recv)
         for r, dd in self.ranks:
             if down and r > 0:
-                buf = got[(r - 1, r)]
-                dd.import_rows(b[r] - 1, 1, buf, buf.numel())
+                dd.import_rows_slab(b[r] - 1, 1, got[(r - 1, r)])
             if not down and r < N - 1:
-                buf = got[(r + 1, r)]
-                dd.import_rows(b[r + 1] - 1, 1, buf, buf.numel())
+                dd.import_rows_slab(b[r + 1] - 1, 1, got[(r + 1, r)])
 
-    def sweep(self):
+    def sweep(self, record=False):
         part = 1 if self.half_index % 2 == 0 else 2
         striped = self.bounds is not None
         nca = self.nb // 2 if part == 1 else self.nb // 2 + 1
@@ -256,14 +349,90 @@ class StripedRun:
             dd.iterate(1)
         if striped and part == 2:
             self._pass_rows(down=False)
+        if record and striped and part == 1:
+            self._record_a_work()
         self.half_index += 1
 
-    def iterate(self, k):
-        for _ in range(k):
-            self.sweep()
+    # -- cost-aware stripes (tools/stripe_balance.py)
+    def _record_a_work(self):
+        """Per A-cell row: the algorithmic MUFU ops of the A-sweep just done
+        (each rank holds its own cells' counts; summed over ranks).  One host
+        synchronisation per eps stage, outside the exchange path."""
+        import torch
+        na = self.nb // 2
+        w = np.zeros(na)
+        for _, dd in self.ranks:
+            _, _, mf, _ = dd.cell_stats()
+            w += mf.reshape(na, na).sum(1)
+        t = self.tr.allreduce_sum(torch.tensor(w, dtype=torch.float64, device=self.device))
+        self.a_work = (self.nb, t.cpu().numpy())
+
+    def rebalance(self):
+        """Before an A-sweep: move the stripe bounds to balance the recorded
+        A-row work (a row moves at most one rank).  Rows change owner with
+        their boxes (dd_export_rows / dd_import_rows + dd_compact); the
+        potentials of both partitions are gathered first, so every rank holds
+        the warm start of the cells it gains.  Per-cell arithmetic is
+        unchanged: the result stays bit-identical to one context."""
+        if self.bounds is None or self.a_work is None or not self.cost_aware:
+            return False
+        nbw, w = self.a_work
+        if nbw != self.nb:                        # recorded on the coarser layer: split each row in two
+            w = np.repeat(w / 2.0, self.nb // nbw)
+        old = list(self.bounds)
+        new = balanced_bounds(self.nb, w, self.nranks, old)
+        if new == old:
+            return False
+        self._gather_alpha()
+        for _, dd in self.ranks:
+            dd.compact()                          # frees the halo slots (the returned boundary row)
+        b, N = old, self.nranks
+        sends, expects, meta = [], [], []
+        for p in range(1, N):
+            if new[p] > old[p]:                   # rows [old_p, new_p) go up: p -> p-1
+                lo, cnt, src, dst = old[p], new[p] - old[p], p, p - 1
+            elif new[p] < old[p]:                 # rows [new_p, old_p) go down: p-1 -> p
+                lo, cnt, src, dst = new[p], old[p] - new[p], p - 1, p
+            else:
+                continue
+            meta.append((lo, cnt, src, dst))
+        for lo, cnt, src, dst in meta:
+            for r, dd in self.ranks:
+                if r == src:
+                    buf = self._export_n(dd, lo, cnt)
+                    sends.append((src, dst, buf))
+            if any(r == dst for r, _ in self.ranks):
+                expects.append((src, dst))
+        got = self.tr.exchange(sends, expects)
+        for lo, cnt, src, dst in meta:
+            for r, dd in self.ranks:
+                if r == dst:
+                    buf = got[(src, dst)]
+                    dd.import_rows(lo, cnt, buf, buf.numel())   # old stripe set: slot by side
+        self.bounds = new
+        for r, dd in self.ranks:
+            dd.set_stripe(new[r], new[r + 1])
+            dd.compact()
+        self.rebalances += 1
+        self._size_slabs()
+        return True
+
+    def _export_n(self, dd, row, nrows):
+        import torch
+        n = dd.export_rows_size(row, nrows)
+        buf = torch.empty(n, dtype=torch.uint8, device=self.device)
+        dd.export_rows(row, nrows, buf)
+        self.exchanged_bytes += n
+        return buf
+
+    def iterate(self, k, record_last_a=False):
+        for j in range(k):
+            last_a = record_last_a and (j == k - 1 or j == k - 2) and self.half_index % 2 == 0
+            self.sweep(record=last_a)
 
     def run_schedule(self, n, coarsest, kappa_final, eps_start=0.0):
         self.half_index = 0
+        self.a_work = None
         self.start()
         side = self.ranks[0][1].state_info()["side"]
         for sd, kappa, sweeps in build_schedule(n, coarsest, kappa_final, eps_start):
@@ -271,7 +440,9 @@ class StripedRun:
                 self.refine()
                 side *= 2
             self.set_eps(kappa / sd**2)
-            self.iterate(sweeps)
+            if self.half_index % 2 == 0:
+                self.rebalance()               # cost-aware bounds from the last stage's A-sweep
+            self.iterate(sweeps, record_last_a=self.cost_aware)
 
     # -- whole-problem quantities (sums over ranks)
     def totals(self):

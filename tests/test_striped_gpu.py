@@ -105,3 +105,30 @@ def test_bench_two_ranks_one_gpu_gloo(mods, tmp_path):
     assert abs(line["final"]["transport_cost"] - c1) <= 1e-12 * c1
     assert line["final"]["l1_x"] <= 1e-6 and line["final"]["l1_y"] <= 1e-6
     assert line["cells_per_step"] == g.totals()["cells"]
+
+
+def test_virtual_stripes_cost_aware_rebalance(mods):
+    """Cost-aware stripe bounds (StripedRun.rebalance: rows move between
+    ranks at eps-stage boundaries, balancing the last A-sweep's work) on the
+    cfg-4 recipe at 128^2 with 4 stripes: bounds do move, and the result is
+    still bit-identical to one context (and to equal-row stripes)."""
+    DD, LocalTransport, StripedRun = mods
+    n, s, nranks = 128, 8, 4
+    mu, nu = gaussian_mixture_image(n, 41, 4), gaussian_mixture_image(n, 42, 4)
+    eps = 0.5 / n**2
+    kw = dict(schedule=1, coarsest_side=8, bcap_main=18)
+    ref = DD(mu, nu, eps, s, **kw)
+    ref.run_schedule()
+    out = {}
+    for ca in (True, False):
+        ctxs = [(r, DD(mu, nu, eps, s, **kw)) for r in range(nranks)]
+        run = StripedRun(ctxs, nranks, LocalTransport(nranks), cost_aware=ca)
+        run.run_schedule(n, 8, 0.5)
+        out[ca] = (run, run.basic_marginals_dense())
+    assert out[True][0].rebalances > 0 and out[False][0].rebalances == 0
+    assert out[True][0].bounds != [0, 4, 8, 12, 16]
+    Dr = ref.basic_marginals_dense()
+    assert np.array_equal(Dr, out[True][1]) and np.array_equal(Dr, out[False][1])
+    cr, _ = ref.primal_cost()
+    cs, _ = out[True][0].primal_cost()
+    assert abs(cr - cs) <= 1e-13 * cr

@@ -58,6 +58,10 @@ struct ddo_ctx {
     long long half_index;
     int last_part;
     ddo_sweep_stats stats;
+    /* general separable cost: c(x,y) = h1(|x1-y1|) + h2(|x2-y2|),
+     * tables over finest-grid pixel differences 0..n_final-1 (NULL: |x-y|^2) */
+    double *h1, *h2;
+    int n_final;
     char err[512];
 };
 
@@ -259,6 +263,7 @@ void ddo_free(ddo_ctx* c) {
     for (int k = 0; k < c->n_layers; ++k) {
         free(c->L[k].mu); free(c->L[k].nu); free(c->L[k].logmu); free(c->L[k].mass_i);
     }
+    free(c->h1); free(c->h2);
     free(c);
 }
 
@@ -309,6 +314,7 @@ int ddo_init(ddo_ctx** out, int n, const double* mu, const double* nu, double ep
     for (int sd = coarsest; sd <= n; sd *= 2) ++nl;
     if (nl > MAX_LAYERS) { set_err(c, "too many layers"); return DDO_EINVAL; }
     c->n_layers = nl;
+    c->n_final = n;
     for (int k = nl - 1; k >= 0; --k) {
         layer_t* L = &c->L[k];
         L->side = coarsest << k;
@@ -401,8 +407,42 @@ static void cell_geometry(const ddo_ctx* c, int part, int cidx, cellgeo_t* G) {
     else { G->yr0 = y0; G->yc0 = x0; G->br = y1 - y0 + 1; G->bc = x1 - x0 + 1; }
 }
 
+/* Ground cost between pixels (r1, c1) and (r2, c2) of a layer of the given side,
+ * [0,1]^2 units, pixel centres: |x-y|^2 (W2), or the separable table
+ * cost h1(|x1-y1|) + h2(|x2-y2|) (ddo_set_cost): a layer pixel difference d is
+ * d * n_final / side finest pixels (centres of coarse pixels are finest-grid
+ * distances apart). */
+static double ground_cost(const ddo_ctx* c, int side, int r1, int c1, int r2, int c2) {
+    if (c->h1) {
+        const int st = c->n_final / side;
+        return c->h1[abs(r1 - r2) * st] + c->h2[abs(c1 - c2) * st];
+    }
+    const double h = 1.0 / side;
+    const double d1 = (r1 - r2) * h, d2 = (c1 - c2) * h;
+    return d1 * d1 + d2 * d2;
+}
+
+int ddo_set_cost(ddo_ctx* c, int n_entries, const double* h1, const double* h2) {
+    if (!c) return DDO_EINVAL;
+    free(c->h1); free(c->h2);
+    c->h1 = c->h2 = NULL;
+    if (!h1 && !h2) return DDO_OK;
+    if (!h1 || !h2 || n_entries != c->n_final) {
+        set_err(c, "ddo_set_cost: two tables of n = %d entries required", c->n_final);
+        return DDO_EINVAL;
+    }
+    for (int d = 0; d < n_entries; ++d)
+        if (!isfinite(h1[d]) || !isfinite(h2[d])) { set_err(c, "ddo_set_cost: non-finite entry %d", d); return DDO_EINVAL; }
+    c->h1 = (double*)malloc(sizeof(double) * n_entries);
+    c->h2 = (double*)malloc(sizeof(double) * n_entries);
+    if (!c->h1 || !c->h2) return DDO_ENOMEM;
+    memcpy(c->h1, h1, sizeof(double) * n_entries);
+    memcpy(c->h2, h2, sizeof(double) * n_entries);
+    return DDO_OK;
+}
+
 /* Dense problem of one composite cell: a = mu_J, b = nu_cell = sum_{i in J} nu_i
- * (Alg. 2 line 8), cost c(x,y) = |x-y|^2 in [0,1]^2 units, f = alpha + eps log mu. */
+ * (Alg. 2 line 8), cost c(x,y) (ground_cost), f = alpha + eps log mu. */
 typedef struct {
     int nx, ny;
     double *a, *b, *C, *f, *g;
@@ -441,6 +481,12 @@ static int build_prob(const ddo_ctx* c, const cellgeo_t* G, const double* alpha,
             }
     }
     for (int x = 0; x < P->nx; ++x) {
+        if (c->h1) {
+            for (int y = 0; y < P->ny; ++y)
+                P->C[(size_t)x * P->ny + y] = ground_cost(c, L->side, G->R0 + x / G->ac, G->C0 + x % G->ac,
+                                                          G->yr0 + y / G->bc, G->yc0 + y % G->bc);
+            continue;
+        }
         double x1 = (G->R0 + x / G->ac + 0.5) * h, x2 = (G->C0 + x % G->ac + 0.5) * h;
         for (int y = 0; y < P->ny; ++y) {
             double y1 = (G->yr0 + y / G->bc + 0.5) * h, y2 = (G->yc0 + y % G->bc + 0.5) * h;
@@ -991,7 +1037,6 @@ int ddo_dual_gap(ddo_ctx* c, double* primal, double* dual, double* rel) {
     ksum_t dsum = {0, 0};
     for (size_t g = 0; g < n2; ++g)
         if (L->mu[g] > 0) ks_add(&dsum, L->mu[g] * ah[g] / eps);
-    double h2 = 1.0 / ((double)side * side);
 #ifdef _OPENMP
     int nt = c->opt.n_threads > 0 ? c->opt.n_threads : omp_get_max_threads();
 #pragma omp parallel for schedule(dynamic, 16) num_threads(nt)
@@ -1002,15 +1047,15 @@ int ddo_dual_gap(ddo_ctx* c, double* primal, double* dual, double* rel) {
         double mx = -INFINITY;
         for (size_t x = 0; x < n2; ++x) {
             if (!(L->mu[x] > 0)) continue;
-            double d1 = (double)((int)(x / side) - y1), d2 = (double)((int)(x % side) - y2);
-            double t = ah[x] / eps + L->logmu[x] - (d1 * d1 + d2 * d2) * h2 / eps;
+            double cxy = ground_cost(c, side, (int)(x / side), (int)(x % side), y1, y2);
+            double t = ah[x] / eps + L->logmu[x] - cxy / eps;
             if (t > mx) mx = t;
         }
         double sm = 0;
         for (size_t x = 0; x < n2; ++x) {
             if (!(L->mu[x] > 0)) continue;
-            double d1 = (double)((int)(x / side) - y1), d2 = (double)((int)(x % side) - y2);
-            sm += exp(ah[x] / eps + L->logmu[x] - (d1 * d1 + d2 * d2) * h2 / eps - mx);
+            double cxy = ground_cost(c, side, (int)(x / side), (int)(x % side), y1, y2);
+            sm += exp(ah[x] / eps + L->logmu[x] - cxy / eps - mx);
         }
         /* v_hat is the density w.r.t. nu (K = exp(-c/eps) mu nu):
          * log v_hat(y) = -LSE_x(log u_hat + log mu - c/eps) */

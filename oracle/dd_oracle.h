@@ -84,6 +84,10 @@ int ddo_build_schedule(int n_final, int coarsest_side, double kappa_final, doubl
 int ddo_init(ddo_ctx** out, int n, const double* mu, const double* nu, double eps,
              int cell_size, const ddo_options* opt);
 int ddo_set_eps(ddo_ctx* c, double eps);
+/* General separable cost: c(x,y) = h1(|x1-y1|) + h2(|x2-y2|)
+ * in [0,1]^2 cost units; h1[d], h2[d] for finest-grid pixel differences d = 0..n-1
+ * (n = the finest side; copied).  Both NULL restores |x-y|^2.  Call before iterating. */
+int ddo_set_cost(ddo_ctx* c, int n_entries, const double* h1, const double* h2);
 int ddo_iterate(ddo_ctx* c, int n_half_iters);
 /* Algorithm 2 lines 8-13 for the listed composite cells of partition `part`
  * only (1 = A, 2 = B; row-major cell index), on the current state; cells of

@@ -64,6 +64,7 @@ typedef struct {
     double eps;
     ddo_options opt;
     double *mu, *nu;            /* kept for dd_reset */
+    double *h1, *h2;            /* dd_set_cost tables (re-applied by dd_reset) */
     int pending_fail;           /* ENOCONV reported at the next dd_synchronize (as on the GPU) */
     shim_stats tot;
     char err[256];
@@ -120,7 +121,7 @@ int dd_init(shim_ctx** out, int n, const double* mu, const double* nu, int cost,
 void dd_free(shim_ctx* c) {
     if (!c) return;
     if (c->o) ddo_free(c->o);
-    free(c->mu); free(c->nu);
+    free(c->mu); free(c->nu); free(c->h1); free(c->h2);
     free(c);
 }
 
@@ -129,7 +130,25 @@ int dd_reset(shim_ctx* c) {
     if (c->o) ddo_free(c->o);
     c->o = NULL;
     c->pending_fail = 0;
-    return ddo_init(&c->o, c->n, c->mu, c->nu, c->eps, c->cell_size, &c->opt);
+    int rc = ddo_init(&c->o, c->n, c->mu, c->nu, c->eps, c->cell_size, &c->opt);
+    if (rc == DDO_OK && c->h1) rc = ddo_set_cost(c->o, c->n, c->h1, c->h2);
+    return rc;
+}
+
+int dd_set_cost(shim_ctx* c, int n_entries, const double* h1, const double* h2) {
+    if (!c || !c->o) return SHIM_EINVAL;
+    int rc = ddo_set_cost(c->o, n_entries, h1, h2);
+    if (rc) return rc;
+    free(c->h1); free(c->h2);
+    c->h1 = c->h2 = NULL;
+    if (h1) {
+        c->h1 = (double*)malloc(sizeof(double) * n_entries);
+        c->h2 = (double*)malloc(sizeof(double) * n_entries);
+        if (!c->h1 || !c->h2) return SHIM_ENOMEM;
+        memcpy(c->h1, h1, sizeof(double) * n_entries);
+        memcpy(c->h2, h2, sizeof(double) * n_entries);
+    }
+    return SHIM_OK;
 }
 
 static void add_totals(shim_ctx* c) {

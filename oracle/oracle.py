@@ -63,6 +63,7 @@ def lib():
         _lib.ddo_build_schedule.argtypes = [i, i, d, d, C.POINTER(i), dp, C.POINTER(i), i]
         _lib.ddo_init.argtypes = [C.POINTER(p), i, dp, dp, d, i, C.POINTER(_Opt)]
         _lib.ddo_set_eps.argtypes = [p, d]
+        _lib.ddo_set_cost.argtypes = [p, i, p, p]
         _lib.ddo_iterate.argtypes = [p, i]
         _lib.ddo_solve_cells.argtypes = [p, i, i, p, p]
         _lib.ddo_solve_cells_par.argtypes = [p, i, i, p, p]
@@ -148,6 +149,16 @@ class Oracle:
 
     def set_eps(self, eps):
         return self._check(lib().ddo_set_eps(self._h, eps), "set_eps")
+
+    def set_cost(self, h1=None, h2=None):
+        """General separable cost c = h1(|x1-y1|) + h2(|x2-y2|): tables over
+        finest-grid pixel differences 0..n-1 in [0,1]^2 cost units; None = |x-y|^2."""
+        if h1 is None:
+            return self._check(lib().ddo_set_cost(self._h, 0, None, None), "set_cost")
+        self._h1 = np.ascontiguousarray(h1, dtype=np.float64)
+        self._h2 = np.ascontiguousarray(h2, dtype=np.float64)
+        return self._check(lib().ddo_set_cost(self._h, self._h1.size, _dp(self._h1), _dp(self._h2)),
+                           "set_cost")
 
     def iterate(self, k=1):
         return self._check(lib().ddo_iterate(self._h, k), "iterate", (OK, ENOCONV))

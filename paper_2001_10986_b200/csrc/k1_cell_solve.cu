@@ -195,15 +195,6 @@ __device__ unsigned long long g_phase[2][16];
 #define PROF_ADD(k, v) do {} while (0)
 #endif
 
-__device__ __forceinline__ float grp_sum(float v, unsigned mask, int G) {
-    for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
-    return v;
-}
-__device__ __forceinline__ float grp_max(float v, unsigned mask, int G) {
-    for (int o = G >> 1; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(mask, v, o));
-    return v;
-}
-
 // One separable log-sum-exp pass.  A task is (o1, outputs o2 = 4j .. 4j+3).
 //   out(o1, o2) = S + log sum_k exp(P(o1,k).hi - C(k - o2) - S + P(o1,k).lo2 ln 2)
 // Y1 : o1 = x1, k = x2, o2 = y2 -> Tt[y2][x1]
@@ -212,6 +203,29 @@ __device__ __forceinline__ float grp_max(float v, unsigned mask, int G) {
 // X2 : o1 = x2, k = y1, o2 = x1 -> FXn[x1][x2] = LM - out, L1 X-error
 // Y1S: as Y1 (exact), also the split weights W[y2][x1] of the two x2 halves
 // Y2S: as Y2 (exact), writes the quadrant partial sums ACC[y1][y2] instead of G
+// Lane groups of G (compile time) lanes split the k-range of a task.  Every
+// lane of a warp runs the same number of tasks (ntask_pad) and the exact /
+// speculative mode is decided per WARP for G > 1, so the group reductions are
+// full-warp xor butterflies (offsets < G stay inside the aligned group; the
+// summation order is that of the group) -- no divergent-mask shuffles.
+template <int G>
+__device__ __forceinline__ float gsum(float v) {
+#pragma unroll
+    for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+template <int G>
+__device__ __forceinline__ float gmax(float v) {
+#pragma unroll
+    for (int o = G >> 1; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+template <int PASS, int NT, int G>
+__device__ __forceinline__ void lse_pass_g(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all,
+                                           float2* Fcur, float2* Fout, double& err_acc, int& fallbacks,
+                                           int& nonfinite);
+
 template <int PASS, int NT>
 __device__ __forceinline__ void lse_pass(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all,
                                          float2* Fcur, float2* Fout, double& err_acc, int& fallbacks,
@@ -219,6 +233,26 @@ __device__ __forceinline__ void lse_pass(const K1Lay& L, const Dims& d, const Gr
     // NT threads take part (a larger block calls it with a smaller NT: the
     // lane-group split, hence the summation order, depends on NT only)
     if (threadIdx.x >= NT) return;
+    int n1, n2;
+    if (PASS == PY1 || PASS == PY1S) { n1 = d.ar; n2 = d.bc; }
+    else if (PASS == PY2 || PASS == PY2S) { n1 = d.bc; n2 = d.br; }
+    else if (PASS == PX1) { n1 = d.br; n2 = d.ac; }
+    else { n1 = d.ac; n2 = d.ar; }
+    const int ntask = n1 * ((n2 + kR - 1) / kR);
+    int G = 1;
+    while (G < 8 && ntask * G * 2 <= NT) G <<= 1;
+    switch (G) {
+    case 1: lse_pass_g<PASS, NT, 1>(L, d, gq, exact_all, Fcur, Fout, err_acc, fallbacks, nonfinite); break;
+    case 2: lse_pass_g<PASS, NT, 2>(L, d, gq, exact_all, Fcur, Fout, err_acc, fallbacks, nonfinite); break;
+    case 4: lse_pass_g<PASS, NT, 4>(L, d, gq, exact_all, Fcur, Fout, err_acc, fallbacks, nonfinite); break;
+    default: lse_pass_g<PASS, NT, 8>(L, d, gq, exact_all, Fcur, Fout, err_acc, fallbacks, nonfinite); break;
+    }
+}
+
+template <int PASS, int NT, int G>
+__device__ __forceinline__ void lse_pass_g(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all,
+                                           float2* Fcur, float2* Fout, double& err_acc, int& fallbacks,
+                                           int& nonfinite) {
     constexpr bool kY1 = (PASS == PY1 || PASS == PY1S);
     constexpr bool kY2 = (PASS == PY2 || PASS == PY2S);
     constexpr bool kSplit = (PASS == PY1S || PASS == PY2S);
@@ -233,10 +267,7 @@ __device__ __forceinline__ void lse_pass(const K1Lay& L, const Dims& d, const Gr
 
     const int n2q = (n2 + kR - 1) / kR;
     const int ntask = n1 * n2q;
-    int G = 1;
-    while (G < 8 && ntask * G * 2 <= NT) G <<= 1;
     const int lg = threadIdx.x & (G - 1);
-    const unsigned gmask = ((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1));
     const int ntask_pad = ((ntask + (NT / G) - 1) / (NT / G)) * (NT / G);
     const float2 L2E2 = make_float2(kL2E, kL2E);
 
@@ -284,7 +315,7 @@ __device__ __forceinline__ void lse_pass(const K1Lay& L, const Dims& d, const Gr
 #pragma unroll
             for (int r = 0; r < kR; ++r) if (skip[r]) S[r] = Sf;
             exact = !okS;
-            if (G > 1) exact = __any_sync(gmask, exact);   // one mode per lane group
+            if (G > 1) exact = __any_sync(0xffffffffu, exact);   // one mode per warp (converged shuffles)
         }
         const float* ctp = L.CT + d.off - o2;   // C(k - o2 - r) = ctp[k - r]
         float acc[kR], acc1[kR], q[kR][4];
@@ -301,7 +332,7 @@ __device__ __forceinline__ void lse_pass(const K1Lay& L, const Dims& d, const Gr
                 }
 #pragma unroll
                 for (int r = 0; r < kR; ++r) {
-                    if (G > 1) M[r] = grp_max(M[r], gmask, G);
+                    if (G > 1) M[r] = gmax<G>(M[r]);
                     if (M[r] == -INFINITY) { skip[r] = true; S[r] = 0.f; }
                     else S[r] = M[r];
                 }
@@ -360,10 +391,11 @@ __device__ __forceinline__ void lse_pass(const K1Lay& L, const Dims& d, const Gr
 #pragma unroll
             for (int r = 0; r < kR; ++r) {
                 if (G > 1) {
-                    acc[r] = grp_sum(acc[r], gmask, G);
-                    acc1[r] = grp_sum(acc1[r], gmask, G);
+                    acc[r] = gsum<G>(acc[r]);
+                    acc1[r] = gsum<G>(acc1[r]);
                     if (PASS == PY2S)
-                        for (int c = 0; c < 4; ++c) q[r][c] = grp_sum(q[r][c], gmask, G);
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) q[r][c] = gsum<G>(q[r][c]);
                 }
                 tot[r] = (PASS == PY2S) ? (q[r][0] + q[r][1]) + (q[r][2] + q[r][3]) : acc[r] + acc1[r];
             }
@@ -373,7 +405,7 @@ __device__ __forceinline__ void lse_pass(const K1Lay& L, const Dims& d, const Gr
             bool ok = true;
 #pragma unroll
             for (int r = 0; r < kR; ++r) ok = ok && (skip[r] || (tot[r] >= 0.25f && tot[r] <= 4.0f));
-            if (G > 1) ok = __all_sync(gmask, ok);
+            if (G > 1) ok = __all_sync(0xffffffffu, ok);
             if (ok) { done = true; break; }
             exact = true;
             if (lg == 0) ++fallbacks;

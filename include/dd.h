@@ -147,6 +147,21 @@ int dd_set_eps(dd_ctx* ctx, double eps);
  * (dd_options.max_inner_iter; reading A6).  k >= 1, else DD_EINVAL. */
 int dd_set_max_inner_iter(dd_ctx* ctx, int k);
 
+/* dd_set_cost -- general separable ground cost (Sec. 7.1 "Test data":
+ * the scheme applies to costs h(x - y)):
+ *   c(x, y) = h1(|x1 - y1|) + h2(|x2 - y2|)   ([0,1]^2 cost units, x1 = row)
+ * h1, h2: host arrays of n entries (n = the finest side), h_k[d] = the cost of a
+ * difference of d finest-grid pixels (d = 0..n-1); copied.  A coarse layer of
+ * side m uses h_k[d * n / m] (pixel centres of the coarse grid are finest-grid
+ * distances apart).  Both NULL restores |x - y|^2.  Call between sweeps (it
+ * synchronises the context).  Numerics: per cell, every table entry / eps is
+ * split into a hi part on the cell's 2^-q grid and a lo remainder (DESIGN.md
+ * "general costs"), so the hi arithmetic of K1 stays exact for any real table.
+ * Scope: general costs (and s = 16) run on the SMEM tier; a cell whose union
+ * Y box exceeds its capacity is flagged and dd_synchronize returns DD_ENOMEM.
+ * Errors: DD_EINVAL (wrong length, one table NULL, non-finite entry). */
+int dd_set_cost(dd_ctx* ctx, int n_entries, const double* h1, const double* h2);
+
 /* dd_refine -- move to the next finer layer: nu_i^0 by eq. FineBasicMarginals
  * (P:1471-1474); alpha warm start = the coarse potentials glued by the
  * discrete Helmholtz least squares and interpolated linearly in

@@ -33,10 +33,22 @@ struct EvalParams {
     int* coo_x;
     int* coo_y;
     double* coo_m;
+    const double* h1;           // general separable cost tables (nullptr: |x-y|^2), SweepParams::h1
+    const double* h2;
+    int hst;
 };
 
+// Ground cost between layer pixels (r1, c1) and (r2, c2), [0,1]^2 units.
+__device__ __forceinline__ double ground_cost(const double* h1, const double* h2, int hst, int side,
+                                              int r1, int c1, int r2, int c2) {
+    if (h1) return h1[(long long)abs(r1 - r2) * hst] + h2[(long long)abs(c1 - c2) * hst];
+    const double h = 1.0 / side;
+    const double d1 = (r1 - r2) * h, d2 = (c1 - c2) * h;
+    return d1 * d1 + d2 * d2;
+}
+
 cudaError_t k1_phase_read(unsigned long long* out32);
-size_t k1_smem_bytes_host(int s, int bcap, bool big = false, int nwarps = 0);
+size_t k1_smem_bytes_host(int s, int bcap, bool big = false, int nwarps = 0, bool gc = false);
 cudaError_t launch_k1(const SweepParams& p, int tier, int grid, size_t smem, cudaStream_t st);
 int k1_max_clusters(size_t smem);
 cudaError_t launch_k0_cluster(const int* sorted, int* counts, int ncap, const int* bside, float theta, int nsm,
@@ -78,7 +90,8 @@ size_t glue_scratch_doubles(int side_c, int s_c);
 cudaError_t launch_glue_phi(const double* aA, const double* aB, const double* mu, int side, int s, double eps,
                             double* scratch, double** phi_out);
 cudaError_t launch_dual_terms(const double* phi, const double* mu, const double* logmu, const double* nu, int n,
-                              double eps, double kappa, double* T, double* term, cudaStream_t st);
+                              double eps, double kappa, double* T, double* term, cudaStream_t st,
+                              const double* h1 = nullptr, const double* h2 = nullptr, int hst = 1);
 cudaError_t launch_mufu_bench(float* out, int blocks, int threads, int iters, cudaStream_t st);
 
 }  // namespace dd

@@ -84,6 +84,12 @@ struct SweepParams {
     int* ipred;           // this partition's iteration counts of the previous sweep (work predictor for the LPT order)
     int poison;           // testing (DD_POISON): K1 fills its dynamic SMEM with 0xFF bytes first
     size_t smem_bytes;    // dynamic SMEM of the launch (for the poison fill)
+    // general separable cost (dd_set_cost): c = h1(|dr|) + h2(|dc|) in [0,1]^2 units,
+    // tables over FINEST-grid pixel differences; a layer difference d is d * hst finest
+    // pixels.  nullptr: |x - y|^2 (the shifted-gauge quadratic path)
+    const double* h1;
+    const double* h2;
+    int hst;
 };
 
 // ------------------------------------------------------------- helpers --

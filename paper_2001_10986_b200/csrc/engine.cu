@@ -103,6 +103,9 @@ struct dd_ctx {
     long long halo_cap = 0;
     long long* d_xoff = nullptr;    // row export/import offsets scratch
     double* glue = nullptr;         // K5 potential refinement scratch
+    // general separable cost (dd_set_cost): finest-grid tables h1 (rows), h2 (columns)
+    double* d_h1 = nullptr;
+    double* d_h2 = nullptr;
     bool serial = false;            // DD_SERIAL_TIERS=1: all K1 tiers on one stream (profiling)
     long long xoff_n = 0;
     // host bookkeeping
@@ -262,6 +265,21 @@ void tier_caps(int s, int opt_main, int opt_big, int* b0, int* b1, int* b2) {
 
 void choose_caps(dd_ctx* c, int s) {
     int b0, b1, b2;
+    if (c->d_h1 || s > 8) {
+        // general costs and s = 16 run on the SMEM tier only (DESIGN.md "general
+        // costs, s = 16"): its box capacity is raised to what one SM holds
+        // (1 CTA/SM at the largest boxes); a cell beyond it is flagged by the
+        // big tiers (DD_ENOMEM), never solved with the wrong arithmetic
+        const bool gc = c->d_h1 != nullptr;
+        int b = std::max(2 * s + 2, 24);
+        while (b < 4096 && k1_smem_bytes_host(s, b + 1, false, 0, gc) <= kSmem2) ++b;
+        c->bcap_main = b;
+        c->smem_main = k1_smem_bytes_host(s, b, false, 0, gc);
+        c->bcap_big = c->bcap_big2 = b;
+        c->smem_big = k1_smem_bytes_host(s < 8 ? s : 8, std::min(b, c->slice_cap[0]), true, kT1Threads / 32);
+        c->smem_big2 = k1_smem_bytes_host(s < 8 ? s : 8, std::min(b, c->slice_cap[1]), true, kT2Threads / 32);
+        return;
+    }
     tier_caps(s, c->opt.reserved[0], c->opt.reserved[1], &b0, &b1, &b2);
     c->bcap_main = b0;
     c->smem_main = k1_smem_bytes_host(s, b0);
@@ -299,6 +317,7 @@ int sweep(dd_ctx* c) {
     p.side = Lr.side; p.s = Lr.s; p.nb = Lr.nb; p.nca = nca; p.ncells = ncells;
     cell_rows(c, part, Lr.nb, &p.cr0, &p.cr1);
     p.eps = c->eps;
+    p.h1 = c->d_h1; p.h2 = c->d_h2; p.hst = c->L[c->n_layers - 1].side / Lr.side;
     p.kappa = c->eps * (double)Lr.side * (double)Lr.side;
     p.tau = c->tau;
     p.err_tol = c->opt.err_tol;
@@ -421,7 +440,8 @@ void free_all(dd_ctx* c) {
     }
     void* ptrs[] = {c->alphaA, c->alphaB, c->box, c->box2, c->off, c->off2, c->pool, c->scratch,
                     c->bump, c->lists, c->bside, c->ipred, c->slices[0], c->slices[1], c->counters, c->cellout, c->d_total, c->d_last, c->d_tot,
-                    c->eval_scratch, c->eval_res, c->d_sums, c->yacc, c->partial, c->d_xoff, c->glue, c->cl_slices};
+                    c->eval_scratch, c->eval_res, c->d_sums, c->yacc, c->partial, c->d_xoff, c->glue, c->cl_slices,
+                    c->d_h1, c->d_h2};
     for (void* q : ptrs) if (q) cudaFree(q);
     for (auto& ev : c->pending) for (int k = 0; k < 3; ++k) cudaEventDestroy(ev.e[k]);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -494,6 +514,7 @@ int evaluate(dd_ctx* c, double* out3, bool coo, long long* coo_count, int* cx, i
     EvalParams p{};
     p.part = part; p.side = Lr.side; p.s = Lr.s; p.nb = Lr.nb; p.nca = nca;
     p.eps = c->eps;
+    p.h1 = c->d_h1; p.h2 = c->d_h2; p.hst = c->L[c->n_layers - 1].side / Lr.side;
     p.box = c->box; p.off = c->off; p.pool = c->pool;
     p.alpha = part == 1 ? c->alphaA : c->alphaB;
     p.mu = Lr.mu; p.logmu = Lr.logmu; p.nu = Lr.nu;
@@ -807,6 +828,30 @@ int dd_reset(dd_ctx* c) {
     c->stripe_lo = c->stripe_hi = 0;
     c->eps = (c->opt.schedule == DD_SCHED_LADDER) ? 2.0 / ((double)c->L[0].side * c->L[0].side) : c->eps_final;
     return product_init(c);
+}
+
+int dd_set_cost(dd_ctx* c, int n_entries, const double* h1, const double* h2) {
+    if (!c) return DD_EINVAL;
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->st));
+    if (c->d_h1) { CK(cudaFree(c->d_h1)); c->d_h1 = nullptr; }
+    if (c->d_h2) { CK(cudaFree(c->d_h2)); c->d_h2 = nullptr; }
+    if (!h1 && !h2) return DD_OK;
+    const int n = c->L[c->n_layers - 1].side;
+    if (!h1 || !h2 || n_entries != n) {
+        set_err(c, "dd_set_cost: two tables of n = %d entries (finest-grid pixel differences) required", n);
+        return DD_EINVAL;
+    }
+    for (int d = 0; d < n; ++d)
+        if (!std::isfinite(h1[d]) || !std::isfinite(h2[d])) {
+            set_err(c, "dd_set_cost: non-finite table entry at d = %d", d);
+            return DD_EINVAL;
+        }
+    CK(cudaMalloc(&c->d_h1, n * sizeof(double)));
+    CK(cudaMalloc(&c->d_h2, n * sizeof(double)));
+    CK(cudaMemcpy(c->d_h1, h1, n * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_h2, h2, n * sizeof(double), cudaMemcpyHostToDevice));
+    return DD_OK;
 }
 
 int dd_set_max_inner_iter(dd_ctx* c, int k) {
@@ -1274,7 +1319,8 @@ int dd_dual_gap(dd_ctx* c, double* primal, double* dual, double* rel_gap) {
     double* T = nullptr;
     CK(cudaMalloc(&T, 2 * n2 * sizeof(double)));
     const double kappa = c->eps * (double)Lr.side * Lr.side;
-    CK(launch_dual_terms(phi, Lr.mu, Lr.logmu, Lr.nu, Lr.side, c->eps, kappa, T, T + n2, c->st));
+    CK(launch_dual_terms(phi, Lr.mu, Lr.logmu, Lr.nu, Lr.side, c->eps, kappa, T, T + n2, c->st,
+                         c->d_h1, c->d_h2, c->L[c->n_layers - 1].side / Lr.side));
     // fixed-order sum of the n^2 terms
     std::vector<double> h(n2);
     CK(cudaMemcpyAsync(h.data(), T + n2, n2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));

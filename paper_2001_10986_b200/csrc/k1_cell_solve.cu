@@ -54,6 +54,8 @@ struct K1Lay {
     int* GL;      // BIG: row groups of the fused pass, heaviest first (dynamic LPT)
     int2* GI;     // BIG: per row group, the union of its rows' non-zero column ranges
     double* errv; // BIG: per X point, the X-error term of the current iteration [a_r][a_c]
+    float2* CG;   // general cost (tier 0 only): 4 tables [row+, row-, col+, col-][2 off + 8] of
+                  // (hi on the cell grid, lo2) -- index semantics as CT, see cg_table()
 };
 
 // BIG mode (fused Y2+X1): G is never stored as
@@ -64,7 +66,8 @@ constexpr int kGbufPerWarp = 144;   // max over NQ (RG = 4) of RG * YS * (SUB + 
 __host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
 __host__ __device__ inline int k1_ct_off(int s, int bcap) { return (2 * s > bcap ? 2 * s : bcap) + 24; }
 
-__host__ __device__ inline void k1_sizes(int s, int bcap, size_t* sz, bool big = false, int nwarps = 0) {
+__host__ __device__ inline void k1_sizes(int s, int bcap, size_t* sz, bool big = false, int nwarps = 0,
+                                         bool gc = false) {
     const size_t A = 2 * s, pA = odd_pitch(2 * s), pB = odd_pitch(bcap), B = bcap;
     sz[0] = align16(A * pA * 8);                        // FX
     sz[1] = align16(A * pA * 8);                        // FXn
@@ -84,20 +87,22 @@ __host__ __device__ inline void k1_sizes(int s, int bcap, size_t* sz, bool big =
     sz[15] = align16((size_t)A * A * 8);                             // errv (fp64 rescue, BIG loop)
     sz[16] = big ? align16((size_t)(bcap + 1) * 8) : 0;             // RI
     sz[17] = big ? align16((size_t)(bcap / 4 + 2) * 4) : 0;         // GL
-    sz[18] = 0;                                                      // (unused)
+    sz[18] = (gc && !big) ? align16((size_t)4 * (2 * k1_ct_off(s, bcap) + 8) * 8) : 0;   // CG
     sz[19] = big ? align16((size_t)(bcap / 4 + 2) * 8) : 0;         // GI
 }
 
-__host__ __device__ inline size_t k1_smem_bytes(int s, int bcap, bool big = false, int nwarps = 0) {
+__host__ __device__ inline size_t k1_smem_bytes(int s, int bcap, bool big = false, int nwarps = 0,
+                                                bool gc = false) {
     size_t sz[20], b = 0;
-    k1_sizes(s, bcap, sz, big, nwarps);
+    k1_sizes(s, bcap, sz, big, nwarps, gc);
     for (int k = 0; k < 20; ++k) b += sz[k];
     return b;
 }
 
-__device__ inline K1Lay k1_carve(unsigned char* base, int s, int bcap, bool big = false, int nwarps = 0) {
+__device__ inline K1Lay k1_carve(unsigned char* base, int s, int bcap, bool big = false, int nwarps = 0,
+                                 bool gc = false) {
     size_t sz[20];
-    k1_sizes(s, bcap, sz, big, nwarps);
+    k1_sizes(s, bcap, sz, big, nwarps, gc);
     K1Lay L;
     size_t o = 0;
     L.FX = (float2*)(base + o);  o += sz[0];
@@ -119,7 +124,7 @@ __device__ inline K1Lay k1_carve(unsigned char* base, int s, int bcap, bool big 
     L.errv = (double*)(base + o); o += sz[15];
     L.RI = (int2*)(base + o); o += sz[16];
     L.GL = (int*)(base + o); o += sz[17];
-    o += sz[18];
+    L.CG = (float2*)(base + o); o += sz[18];
     L.GI = (int2*)(base + o);
     return L;
 }
@@ -221,12 +226,12 @@ __device__ __forceinline__ float gmax(float v) {
     return v;
 }
 
-template <int PASS, int NT, int G>
+template <int PASS, int NT, int G, bool GC>
 __device__ __forceinline__ void lse_pass_g(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all,
                                            float2* Fcur, float2* Fout, double& err_acc, int& fallbacks,
                                            int& nonfinite);
 
-template <int PASS, int NT>
+template <int PASS, int NT, bool GC = false>
 __device__ __forceinline__ void lse_pass(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all,
                                          float2* Fcur, float2* Fout, double& err_acc, int& fallbacks,
                                          int& nonfinite) {
@@ -242,14 +247,14 @@ __device__ __forceinline__ void lse_pass(const K1Lay& L, const Dims& d, const Gr
     int G = 1;
     while (G < 8 && ntask * G * 2 <= NT) G <<= 1;
     switch (G) {
-    case 1: lse_pass_g<PASS, NT, 1>(L, d, gq, exact_all, Fcur, Fout, err_acc, fallbacks, nonfinite); break;
-    case 2: lse_pass_g<PASS, NT, 2>(L, d, gq, exact_all, Fcur, Fout, err_acc, fallbacks, nonfinite); break;
-    case 4: lse_pass_g<PASS, NT, 4>(L, d, gq, exact_all, Fcur, Fout, err_acc, fallbacks, nonfinite); break;
-    default: lse_pass_g<PASS, NT, 8>(L, d, gq, exact_all, Fcur, Fout, err_acc, fallbacks, nonfinite); break;
+    case 1: lse_pass_g<PASS, NT, 1, GC>(L, d, gq, exact_all, Fcur, Fout, err_acc, fallbacks, nonfinite); break;
+    case 2: lse_pass_g<PASS, NT, 2, GC>(L, d, gq, exact_all, Fcur, Fout, err_acc, fallbacks, nonfinite); break;
+    case 4: lse_pass_g<PASS, NT, 4, GC>(L, d, gq, exact_all, Fcur, Fout, err_acc, fallbacks, nonfinite); break;
+    default: lse_pass_g<PASS, NT, 8, GC>(L, d, gq, exact_all, Fcur, Fout, err_acc, fallbacks, nonfinite); break;
     }
 }
 
-template <int PASS, int NT, int G>
+template <int PASS, int NT, int G, bool GC>
 __device__ __forceinline__ void lse_pass_g(const K1Lay& L, const Dims& d, const Grid& gq, bool exact_all,
                                            float2* Fcur, float2* Fout, double& err_acc, int& fallbacks,
                                            int& nonfinite) {
@@ -318,6 +323,10 @@ __device__ __forceinline__ void lse_pass_g(const K1Lay& L, const Dims& d, const 
             if (G > 1) exact = __any_sync(0xffffffffu, exact);   // one mode per warp (converged shuffles)
         }
         const float* ctp = L.CT + d.off - o2;   // C(k - o2 - r) = ctp[k - r]
+        // general cost: the pass's (axis, orientation) table, same indexing,
+        // entries (hi on the cell grid, lo2 = (C - hi) log2 e)
+        constexpr int kTab = kY1 ? 2 : kY2 ? 0 : (PASS == PX1) ? 3 : 1;
+        const float2* cgp = GC ? L.CG + kTab * (2 * d.off + 8) + d.off - o2 : nullptr;
         float acc[kR], acc1[kR], q[kR][4];
         bool done = false;
         for (int attempt = 0; attempt < 2 && !done; ++attempt) {
@@ -328,7 +337,7 @@ __device__ __forceinline__ void lse_pass_g(const K1Lay& L, const Dims& d, const 
                 for (int k = lg; k < K; k += G) {
                     const float px = Prow[k].x;
 #pragma unroll
-                    for (int r = 0; r < kR; ++r) M[r] = fmaxf(M[r], px - ctp[k - r]);
+                    for (int r = 0; r < kR; ++r) M[r] = fmaxf(M[r], px - (GC ? cgp[k - r].x : ctp[k - r]));
                 }
 #pragma unroll
                 for (int r = 0; r < kR; ++r) {
@@ -346,6 +355,31 @@ __device__ __forceinline__ void lse_pass_g(const K1Lay& L, const Dims& d, const 
             // ---- the hot loop: 4 exps per 8-byte P load + 1 cost-table load
             auto body = [&](int k, float c0, float c1, float c2, float c3, float* A, int half) {
                 const float2 pk = Prow[k];
+                if constexpr (GC) {      // c_r = the hi parts; the lo parts join the lo term
+                    const float2 g0 = cgp[k], g1 = cgp[k - 1], g2 = cgp[k - 2], g3 = cgp[k - 3];
+                    c0 = g0.x; c1 = g1.x; c2 = g2.x; c3 = g3.x;
+                    float2 t01 = __fadd2_rn(make_float2(pk.x, pk.x), make_float2(-c0, -c1));
+                    float2 t23 = __fadd2_rn(make_float2(pk.x, pk.x), make_float2(-c2, -c3));
+                    t01 = __fadd2_rn(t01, nS01);
+                    t23 = __fadd2_rn(t23, nS23);
+                    t01 = __ffma2_rn(t01, L2E2, make_float2(pk.y - g0.y, pk.y - g1.y));
+                    t23 = __ffma2_rn(t23, L2E2, make_float2(pk.y - g2.y, pk.y - g3.y));
+                    const float e0 = ex2f(t01.x), e1 = ex2f(t01.y), e2 = ex2f(t23.x), e3 = ex2f(t23.y);
+                    if (PASS == PY2S) {
+                        const float2 w = Wb[o1 * d.pT + k];
+                        const int c = 2 * half;
+                        q[0][c] = fmaf(e0, w.x, q[0][c]); q[0][c + 1] = fmaf(e0, w.y, q[0][c + 1]);
+                        q[1][c] = fmaf(e1, w.x, q[1][c]); q[1][c + 1] = fmaf(e1, w.y, q[1][c + 1]);
+                        q[2][c] = fmaf(e2, w.x, q[2][c]); q[2][c + 1] = fmaf(e2, w.y, q[2][c + 1]);
+                        q[3][c] = fmaf(e3, w.x, q[3][c]); q[3][c + 1] = fmaf(e3, w.y, q[3][c + 1]);
+                    } else {
+                        float2 a01 = make_float2(A[0], A[1]), a23 = make_float2(A[2], A[3]);
+                        a01 = __fadd2_rn(a01, make_float2(e0, e1));
+                        a23 = __fadd2_rn(a23, make_float2(e2, e3));
+                        A[0] = a01.x; A[1] = a01.y; A[2] = a23.x; A[3] = a23.y;
+                    }
+                    return;
+                }
                 float2 t01 = __fadd2_rn(make_float2(pk.x, pk.x), make_float2(-c0, -c1));
                 float2 t23 = __fadd2_rn(make_float2(pk.x, pk.x), make_float2(-c2, -c3));
                 t01 = __fadd2_rn(t01, nS01);
@@ -367,7 +401,11 @@ __device__ __forceinline__ void lse_pass_g(const K1Lay& L, const Dims& d, const 
                     A[0] = a01.x; A[1] = a01.y; A[2] = a23.x; A[3] = a23.y;
                 }
             };
-            if (G == 1) {
+            if (GC) {
+                for (int k = lg; k < ksplit; k += G) body(k, 0.f, 0.f, 0.f, 0.f, acc, 0);
+                const int k1 = ksplit + ((lg - ksplit % G) % G + G) % G;
+                for (int k = k1; k < K; k += G) body(k, 0.f, 0.f, 0.f, 0.f, acc1, 1);
+            } else if (G == 1) {
                 // sliding cost window: c_r = C(k - o2 - r)
                 float c1 = ctp[-1], c2 = ctp[-2], c3 = ctp[-3];
 #pragma unroll 2
@@ -1088,15 +1126,34 @@ __device__ void final_split_big(const K1Lay& L, const Dims& d, float4* __restric
 // solver cannot finish is Sec. 7.3.)
 constexpr int kRescueIters = 2048;
 
+// Per-axis cost in eps units for a LOCAL index difference e of a pass, by
+// table t (0 row+: e = x1 - y1, 1 row-: e = y1 - x1, 2 col+: e = x2 - y2,
+// 3 col-: e = y2 - x2): the global pixel difference is +-e + D (D = X-box
+// origin - Y-box origin).  Quadratic: e^2 / kappa in the shifted gauge
+// (DESIGN.md), symmetric, so t does not matter.  General (dd_set_cost,
+// P:1528): h1 (rows) / h2 (columns) at |+-e + D| * hst finest pixels.
+struct CostF {
+    double ik, ie;
+    const double* h1;
+    const double* h2;
+    int hst, side, Dr, Dc;
+    __device__ double operator()(int t, int e) const {
+        if (!h1) { const double v = (double)e; return v * v * ik; }
+        int g = (t & 1) ? -e : e;
+        g += (t < 2) ? Dr : Dc;
+        g = min(abs(g), side - 1);
+        return ((t < 2) ? h1 : h2)[(long long)g * hst] * ie;
+    }
+};
+
 template <int NT>
 __device__ int rescue_fp64(const K1Lay& L, const Dims& d, double* F, double* Fn, double* G64, int gstr,
-                           const double* LNU64, int lstr, double inv_kappa, double tol, int max_it, double& err) {
+                           const double* LNU64, int lstr, const CostF& cf, double tol, int max_it, double& err) {
     constexpr int NR = 256;
     const int tid = threadIdx.x;
     const bool act = tid < NR;
     double* T = reinterpret_cast<double*>(L.Tt);     // [y2][pT]
     double* U = reinterpret_cast<double*>(L.Ut);     // [x2][pU]
-    auto C = [inv_kappa](int k) { const double v = (double)k; return v * v * inv_kappa; };
     int n = 0;
     while (true) {
         // Y1: T(x1, y2) = LSE_x2 [F(x1, x2) - C(x2 - y2)]
@@ -1104,10 +1161,10 @@ __device__ int rescue_fp64(const K1Lay& L, const Dims& d, double* F, double* Fn,
             const int x1 = o % d.ar, y2 = o / d.ar;
             const double* Fr = F + x1 * d.pX;
             double M = -INFINITY;
-            for (int x2 = 0; x2 < d.ac; ++x2) M = fmax(M, Fr[x2] - C(x2 - y2));
+            for (int x2 = 0; x2 < d.ac; ++x2) M = fmax(M, Fr[x2] - cf(2, x2 - y2));
             double sm = 0.0;
             if (M > -INFINITY)
-                for (int x2 = 0; x2 < d.ac; ++x2) sm += exp(Fr[x2] - C(x2 - y2) - M);
+                for (int x2 = 0; x2 < d.ac; ++x2) sm += exp(Fr[x2] - cf(2, x2 - y2) - M);
             T[y2 * d.pT + x1] = M > -INFINITY ? M + log(sm) : -INFINITY;
         }
         __syncthreads();
@@ -1119,9 +1176,9 @@ __device__ int rescue_fp64(const K1Lay& L, const Dims& d, double* F, double* Fn,
             if (ln > -INFINITY) {
                 const double* Tc = T + y2 * d.pT;
                 double M = -INFINITY;
-                for (int x1 = 0; x1 < d.ar; ++x1) M = fmax(M, Tc[x1] - C(x1 - y1));
+                for (int x1 = 0; x1 < d.ar; ++x1) M = fmax(M, Tc[x1] - cf(0, x1 - y1));
                 double sm = 0.0;
-                for (int x1 = 0; x1 < d.ar; ++x1) sm += exp(Tc[x1] - C(x1 - y1) - M);
+                for (int x1 = 0; x1 < d.ar; ++x1) sm += exp(Tc[x1] - cf(0, x1 - y1) - M);
                 g = ln - (M + log(sm));
             }
             G64[(size_t)o * gstr] = g;
@@ -1132,10 +1189,10 @@ __device__ int rescue_fp64(const K1Lay& L, const Dims& d, double* F, double* Fn,
             const int y1 = o % d.br, x2 = o / d.br;
             const double* Gr = G64 + (size_t)y1 * d.bc * gstr;
             double M = -INFINITY;
-            for (int y2 = 0; y2 < d.bc; ++y2) M = fmax(M, Gr[(size_t)y2 * gstr] - C(y2 - x2));
+            for (int y2 = 0; y2 < d.bc; ++y2) M = fmax(M, Gr[(size_t)y2 * gstr] - cf(3, y2 - x2));
             double sm = 0.0;
             if (M > -INFINITY)
-                for (int y2 = 0; y2 < d.bc; ++y2) sm += exp(Gr[(size_t)y2 * gstr] - C(y2 - x2) - M);
+                for (int y2 = 0; y2 < d.bc; ++y2) sm += exp(Gr[(size_t)y2 * gstr] - cf(3, y2 - x2) - M);
             U[x2 * d.pU + y1] = M > -INFINITY ? M + log(sm) : -INFINITY;
         }
         __syncthreads();
@@ -1148,10 +1205,10 @@ __device__ int rescue_fp64(const K1Lay& L, const Dims& d, double* F, double* Fn,
             if (lm > -INFINITY) {
                 const double* Ur = U + x2 * d.pU;
                 double M = -INFINITY;
-                for (int y1 = 0; y1 < d.br; ++y1) M = fmax(M, Ur[y1] - C(y1 - x1));
+                for (int y1 = 0; y1 < d.br; ++y1) M = fmax(M, Ur[y1] - cf(1, y1 - x1));
                 double sm = 0.0;
                 if (M > -INFINITY)
-                    for (int y1 = 0; y1 < d.br; ++y1) sm += exp(Ur[y1] - C(y1 - x1) - M);
+                    for (int y1 = 0; y1 < d.br; ++y1) sm += exp(Ur[y1] - cf(1, y1 - x1) - M);
                 fn = M > -INFINITY ? lm - (M + log(sm)) : -INFINITY;
                 const double f = F[x1 * d.pX + x2];
                 e = (fn > -INFINITY && f > -INFINITY) ? (double)L.MU[o] * fabs(expm1(f - fn)) : 0.0;
@@ -1187,7 +1244,9 @@ __device__ int rescue_fp64(const K1Lay& L, const Dims& d, double* F, double* Fn,
 template <int NT, bool BIG, int CS>
 __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, unsigned char* gslice) {
     static_assert(CS == 1 || BIG, "cluster tier = big-cell path");
-    const K1Lay L = k1_carve(base, p.s, p.bcap, BIG, NT / 32);
+    // general costs (dd_set_cost) run on the SMEM tier only
+    const bool gc = !BIG && p.h1 != nullptr;
+    const K1Lay L = k1_carve(base, p.s, p.bcap, BIG, NT / 32, gc);
     const int rank = CS > 1 ? (int)cluster_rank() : 0;
     __shared__ int4 s_box[4];
     __shared__ long long s_off[4];
@@ -1249,7 +1308,8 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     // local <-> global offsets inside the X and Y boxes
     auto goff = [tr](int r, int c, int& gr, int& gc) { if (tr) { gr = c; gc = r; } else { gr = r; gc = c; } };
     auto qloc = [tr](int q) { return tr ? (((q & 1) << 1) | (q >> 1)) : q; };   // member quadrant, local frame
-    if (d.br > p.bcap || d.bc > p.bcap || d.br == 0 || (BIG && (d.ac % 4 != 0 || d.ar > 16 || d.ac > 16))) {
+    if (d.br > p.bcap || d.bc > p.bcap || d.br == 0 || (BIG && (d.ac % 4 != 0 || d.ar > 16 || d.ac > 16)) ||
+        (BIG && p.h1 != nullptr)) {
         if (tid == 0) {
             co.flags = 2;   // misrouted (tier classification) or empty support
             atomicOr(p.overflow, 2);
@@ -1262,6 +1322,9 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     const int Dr = R0 - Y0, Dc = C0 - X0;          // local-frame offsets (DESIGN.md gauge)
     const double inv_kappa = 1.0 / p.kappa;
     const double inv_eps = 1.0 / p.eps;
+    CostF cf;
+    cf.ik = inv_kappa; cf.ie = inv_eps; cf.h1 = gc ? p.h1 : nullptr; cf.h2 = p.h2; cf.hst = p.hst;
+    cf.side = p.side; cf.Dr = Dr; cf.Dc = Dc;
 
     // ---- cost table (exact for kappa = 2^k)
     for (int i = tid; i < 2 * d.off + 1; i += NT) {
@@ -1284,7 +1347,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         const double m = p.mu[g];
         muJ += m;
         if (m > 0.0) {
-            const double sh = ((2.0 * xr + Dr) * Dr + (2.0 * xc + Dc) * Dc) * inv_kappa;
+            const double sh = gc ? 0.0 : ((2.0 * xr + Dr) * Dr + (2.0 * xc + Dc) * Dc) * inv_kappa;
             const double F = p.alpha[g] * inv_eps + p.logmu[g] - sh;
             fmax_l = fmax(fmax_l, F);
             fmin_l = fmin(fmin_l, F);
@@ -1315,12 +1378,27 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     Grid gq;
     {
         const double dmax = (double)max(d.ar + d.br, d.ac + d.bc);
-        const double M = 2.0 * dmax * dmax * inv_kappa + 2.0 * frange + 64.0;
+        double cmax = dmax * dmax * inv_kappa;
+        if (gc) {     // the largest entry of the cell's four general-cost tables
+            double cm = 0.0;
+            for (int i = tid; i < 4 * (2 * d.off + 1); i += NT) cm = fmax(cm, cf(i / (2 * d.off + 1), i % (2 * d.off + 1) - d.off));
+            cmax = block_max(cm, L.red);
+        }
+        const double M = 2.0 * cmax + 2.0 * frange + 64.0;
         int q = 8;
         while (q > -4 && ldexp(M, q) >= 4194304.0) --q;      // 2 M 2^q < 2^23
         gq.magic = (float)ldexp(1.5, 23 - q);
         gq.scale = ldexp(1.0, q);
         gq.inv = ldexp(1.0, -q);
+    }
+    if (gc) {
+        // general cost tables: hi on the cell grid (so hi - C - S stays exact,
+        // as for the quadratic table), the remainder as lo2 joins the lo term
+        const int tl = 2 * d.off + 8;
+        for (int i = tid; i < 4 * tl; i += NT) {
+            const int t = i / tl, k = i % tl;
+            L.CG[i] = (k <= 2 * d.off) ? split_hl(cf(t, k - d.off), gq) : make_float2(0.f, 0.f);
+        }
     }
     for (int x = tid; x < nx; x += NT) {
         int xr, xc;
@@ -1329,7 +1407,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         const double m = p.mu[g];
         float2 f = make_float2(-INFINITY, 0.f), lm = make_float2(-INFINITY, 0.f);
         if (m > 0.0) {
-            const double sh = ((2.0 * xr + Dr) * Dr + (2.0 * xc + Dc) * Dc) * inv_kappa;
+            const double sh = gc ? 0.0 : ((2.0 * xr + Dr) * Dr + (2.0 * xc + Dc) * Dc) * inv_kappa;
             f = split_hl(p.alpha[g] * inv_eps + p.logmu[g] - sh - lambda, gq);
             lm = split_hl(p.logmu[g], gq);
         }
@@ -1439,6 +1517,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         double e_loc = 0.0;
         PROF_T(ta);
         if (BIG) y1_big<NT, CS>(L, d, gq, exact, fallbacks, nonfinite);
+        else if (gc) lse_pass<PY1, NT, true>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
         else lse_pass<PY1, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
         PROF_T(tb);
         cta_or_cluster_sync<CS>();
@@ -1446,9 +1525,11 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         if (BIG) {
             fused_dispatch<NT, CS>(L, d, gq, exact, LNU, SLg, fallbacks, nonfinite);
         } else {
-            lse_pass<PY2, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
+            if (gc) lse_pass<PY2, NT, true>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
+            else lse_pass<PY2, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
             __syncthreads();
-            lse_pass<PX1, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
+            if (gc) lse_pass<PX1, NT, true>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
+            else lse_pass<PX1, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
         }
         PROF_T(td);
         cta_or_cluster_sync<CS>();
@@ -1456,7 +1537,8 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         if (BIG) {
             x2_finalize<NT, CS>(L, d, gq, Fc, Fn, fallbacks, nonfinite);
         } else {
-            lse_pass<PX2, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
+            if (gc) lse_pass<PX2, NT, true>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
+            else lse_pass<PX2, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
         }
         PROF_T(tf);
         if (BIG) {
@@ -1529,7 +1611,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         // few hundred (measured 257); a cell that is merely this slow in fp64
         // too (the oracle needs > 4e4 iterations on such cells) keeps its
         // Y-feasible plan and is flagged (reading A6)
-        const int n = rescue_fp64<NT>(L, d, F64, Fn64, G64, str, LNU64, str, inv_kappa, tol,
+        const int n = rescue_fp64<NT>(L, d, F64, Fn64, G64, str, LNU64, str, cf, tol,
                                       max(1, min(kRescueIters, p.max_iter - it)), e64);
         it += n;
         err = e64;
@@ -1547,9 +1629,11 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     {
         double dummy = 0.0;
         // (the big-cell path: 256 threads, whatever the CTA shape)
-        lse_pass<PY1S, BIG ? 256 : NT>(L, d, gq, true, Fc, Fn, dummy, fallbacks, nonfinite);
+        if (gc) lse_pass<PY1S, NT, true>(L, d, gq, true, Fc, Fn, dummy, fallbacks, nonfinite);
+        else lse_pass<PY1S, BIG ? 256 : NT>(L, d, gq, true, Fc, Fn, dummy, fallbacks, nonfinite);
         __syncthreads();
         if (BIG) final_split_big<NT>(L, d, ACCp);
+        else if (gc) lse_pass<PY2S, NT, true>(L, d, gq, true, Fc, Fn, dummy, fallbacks, nonfinite);
         else lse_pass<PY2S, NT>(L, d, gq, true, Fc, Fn, dummy, fallbacks, nonfinite);
     }
     if (nonfinite) atomicOr(&s_flag, 2);
@@ -1700,7 +1784,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         const float2 f = Fc[(x / d.ac) * d.pX + x % d.ac];
         double a = 0.0;
         if (f.x > -INFINITY && p.mu[g] > 0.0) {
-            const double sh = ((2.0 * xr + Dr) * Dr + (2.0 * xc + Dc) * Dc) * inv_kappa;
+            const double sh = gc ? 0.0 : ((2.0 * xr + Dr) * Dr + (2.0 * xc + Dc) * Dc) * inv_kappa;
             a = p.eps * (join_hl(f) + lambda + sh - p.logmu[g]);
         }
         p.alpha[g] = a;
@@ -1881,7 +1965,7 @@ cudaError_t launch_k0_cluster(const int* sorted, int* counts, int ncap, const in
     return cudaGetLastError();
 }
 
-size_t k1_smem_bytes_host(int s, int bcap, bool big, int nwarps) { return k1_smem_bytes(s, bcap, big, nwarps); }
+size_t k1_smem_bytes_host(int s, int bcap, bool big, int nwarps, bool gc) { return k1_smem_bytes(s, bcap, big, nwarps, gc); }
 
 cudaError_t launch_k0(const SweepParams& p, int b0, int b1, int* lists, int* counts, int ncap, int* bside,
                       int* sorted, cudaStream_t st) {

@@ -402,16 +402,15 @@ __global__ void k_eval_cells(EvalParams p) {
     for (int y = tid; y < ny; y += blockDim.x) {
         if (!(nuc[y] > 0.0)) { g[y] = -INFINITY; continue; }
         const double yy1 = (y0 + y / bc + 0.5) * h, yy2 = (x0 + y % bc + 0.5) * h;
+        auto cxy = [&](int x) {
+            if (p.h1) return ground_cost(p.h1, p.h2, p.hst, p.side, R0 + x / ac, C0 + x % ac, y0 + y / bc, x0 + y % bc);
+            const double d1 = (R0 + x / ac + 0.5) * h - yy1, d2 = (C0 + x % ac + 0.5) * h - yy2;
+            return d1 * d1 + d2 * d2;
+        };
         double m = -INFINITY;
-        for (int x = 0; x < nx; ++x) {
-            const double d1 = (R0 + x / ac + 0.5) * h - yy1, d2 = (C0 + x % ac + 0.5) * h - yy2;
-            m = fmax(m, f[x] - (d1 * d1 + d2 * d2));
-        }
+        for (int x = 0; x < nx; ++x) m = fmax(m, f[x] - cxy(x));
         double s = 0.0;
-        for (int x = 0; x < nx; ++x) {
-            const double d1 = (R0 + x / ac + 0.5) * h - yy1, d2 = (C0 + x % ac + 0.5) * h - yy2;
-            s += exp((f[x] - (d1 * d1 + d2 * d2) - m) / eps);
-        }
+        for (int x = 0; x < nx; ++x) s += exp((f[x] - cxy(x) - m) / eps);
         g[y] = eps * log(nuc[y]) - (m + eps * log(s));
     }
     __syncthreads();
@@ -432,7 +431,8 @@ __global__ void k_eval_cells(EvalParams p) {
                 }
                 const int gy = y0 + y / bc, gx = x0 + y % bc;
                 const double d1 = xx1 - (gy + 0.5) * h, d2 = xx2 - (gx + 0.5) * h;
-                const double c = d1 * d1 + d2 * d2;
+                const double c = p.h1 ? ground_cost(p.h1, p.h2, p.hst, p.side, R0 + x / ac, C0 + x % ac, gy, gx)
+                                      : d1 * d1 + d2 * d2;
                 const double pi = exp((f[x] + g[y] - c) / eps);
                 const long long gyi = (long long)gy * p.side + gx;
                 px += pi;

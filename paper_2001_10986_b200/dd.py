@@ -21,7 +21,7 @@ FLAG_DEVICE_INPUT = 1
 PLAN_BASIC_MARGINALS, PLAN_COO = 0, 1
 
 # every symbol include/dd.h declares (checked by tests/test_abi.py)
-EXPORTS = ["dd_init", "dd_iterate", "dd_set_eps", "dd_set_max_inner_iter", "dd_refine", "dd_run_schedule", "dd_run_schedule_batch", "dd_reset",
+EXPORTS = ["dd_init", "dd_iterate", "dd_set_eps", "dd_set_max_inner_iter", "dd_set_cost", "dd_refine", "dd_run_schedule", "dd_run_schedule_batch", "dd_reset",
            "dd_primal_cost", "dd_dual_gap", "dd_marginal_error", "dd_fetch_plan", "dd_get_stats", "dd_get_totals",
            "dd_reset_totals", "dd_set_stripe", "dd_clear_rows", "dd_export_rows",
            "dd_import_rows", "dd_export_rows_slab", "dd_import_rows_slab", "dd_compact", "dd_copy_alpha", "dd_y_accumulate", "dd_y_l1", "dd_phase_profile", "dd_get_cell_stats", "dd_get_state_info", "dd_get_state", "dd_set_state",
@@ -70,6 +70,7 @@ def lib():
         L.dd_init.argtypes = [C.POINTER(p), i, p, p, i, d, i, C.POINTER(Options)]
         L.dd_iterate.argtypes = [p, i]
         L.dd_set_eps.argtypes = [p, d]
+        L.dd_set_cost.argtypes = [p, i, p, p]
         if hasattr(L, "dd_set_max_inner_iter"):
             L.dd_set_max_inner_iter.argtypes = [p, i]
         L.dd_refine.argtypes = [p]
@@ -210,6 +211,16 @@ class DD:
 
     def set_eps(self, eps):
         return self._check(lib().dd_set_eps(self._h, eps), "set_eps")
+
+    def set_cost(self, h1=None, h2=None):
+        """General separable cost c = h1(|x1-y1|) + h2(|x2-y2|): tables over
+        finest-grid pixel differences 0..n-1, [0,1]^2 cost units; None = |x-y|^2."""
+        if h1 is None:
+            return self._check(lib().dd_set_cost(self._h, 0, None, None), "set_cost")
+        h1 = np.ascontiguousarray(h1, dtype=np.float64)
+        h2 = np.ascontiguousarray(h2, dtype=np.float64)
+        return self._check(lib().dd_set_cost(self._h, h1.size, h1.ctypes.data_as(C.c_void_p),
+                                             h2.ctypes.data_as(C.c_void_p)), "set_cost")
 
     def set_max_inner_iter(self, k):
         return self._check(lib().dd_set_max_inner_iter(self._h, k), "set_max_inner_iter")

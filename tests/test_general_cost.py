@@ -153,3 +153,156 @@ def test_set_cost_validation():
     h1[3] = np.nan
     with pytest.raises(RuntimeError):
         o.set_cost(h1, h2)
+
+
+# ------------------------------------------------------------------- GPU --
+@pytest.fixture(scope="module")
+def DD():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2001_10986_b200 import DD as _DD
+    return _DD
+
+
+def _mass_i(mu, s):
+    nb = mu.shape[0] // s
+    return mu.reshape(nb, s, nb, s).sum((1, 3)).ravel()
+
+
+@pytest.mark.gpu
+def test_gpu_general_cost_sweeps_vs_oracle(DD):
+    """32^2, s = 4, eps = 2 h^2 with the anisotropic non-quadratic tables:
+    per-sweep basic-cell marginals (P9) and the final gates."""
+    from ddinputs import config_images
+    n, s = 32, 4
+    mu, nu = config_images(1)
+    h1, h2 = cost_tables(n)
+    eps = 2.0 / n**2
+    g = DD(mu, nu, eps, s, err_tol=1e-6)
+    o = Oracle(mu, nu, eps, s, err_tol=1e-6)
+    g.set_cost(h1, h2)
+    o.set_cost(h1, h2)
+    mass = _mass_i(mu, s)
+    for sweep in range(8):
+        g.iterate(1)
+        o.iterate(1)
+        Dg, Do = g.basic_marginals_dense(), o.basic_marginals_dense()
+        diff = np.abs(Dg - Do).sum(1)
+        assert (diff <= 4e-6 * np.maximum(mass, 1e-3)).all(), (sweep, diff.max())
+        assert np.abs(Dg.sum(0) - nu.ravel()).sum() < 1e-11
+    cg, _ = g.primal_cost()
+    co, _ = o.primal_cost()
+    assert abs(cg - co) <= 1e-5 * co, (cg, co)
+    lx, ly = g.marginal_error()
+    assert lx <= 1e-6 and ly <= 1e-6
+    assert g.stats()["failed"] == 0
+
+
+@pytest.mark.gpu
+def test_gpu_general_cost_ladder_vs_oracle(DD):
+    """The cfg-2 ladder (16^2 -> 64^2, eps from 1.0 to 0.5 h^2) with the
+    general cost, both warm-started the same way: final cost, marginals and
+    the PD gap (glued dual with the general cost on both sides)."""
+    from ddinputs import config_images
+    from oracle.oracle import SCHED_LADDER as O_LADDER
+    n = 64
+    mu, nu = config_images(2)
+    h1, h2 = cost_tables(n)
+    eps = 0.5 / n**2
+    g = DD(mu, nu, eps, 4, schedule=1, err_tol=1e-6, eps_start=1.0, coarsest_side=16)
+    o = Oracle(mu, nu, eps, 4, schedule=O_LADDER, err_tol=1e-6, eps_start=1.0, coarsest_side=16,
+               warm_refine=True)
+    g.set_cost(h1, h2)
+    o.set_cost(h1, h2)
+    g.run_schedule()
+    o.run_schedule()
+    cg, _ = g.primal_cost()
+    co, _ = o.primal_cost()
+    assert abs(cg - co) <= 1e-5 * co, (cg, co)
+    lx, ly = g.marginal_error()
+    assert lx <= 1e-6 and ly <= 1e-6
+    rg = g.dual_gap()[2]
+    ro = o.dual_gap()[2]
+    assert -1e-7 < rg < 1e-3 and abs(rg - ro) <= 1e-4 + 0.5 * abs(ro), (rg, ro)
+
+
+@pytest.mark.gpu
+def test_gpu_general_cost_pd_gap_same_state(DD):
+    """The oracle's state imported into the GPU library: primal score and
+    glued dual objective with the general cost agree to 1e-10 (evaluation
+    kernels K7 and k_dual with the tables)."""
+    from ddinputs import config_images
+    n = 32
+    mu, nu = config_images(1)
+    h1, h2 = cost_tables(n)
+    eps = 2.0 / n**2
+    o = Oracle(mu, nu, eps, 4, err_tol=1e-8)
+    o.set_cost(h1, h2)
+    o.iterate(6)
+    Po, Do, ro = o.dual_gap()
+    g = DD(mu, nu, eps, 4, err_tol=1e-8)
+    g.set_cost(h1, h2)
+    g.set_state(o.get_state())
+    Pg, Dg, rg = g.dual_gap()
+    assert abs(Pg - Po) <= 1e-10 * abs(Po)
+    assert abs(Dg - Do) <= 1e-10 * abs(Do)
+    assert g.primal_cost()[0] == pytest.approx(o.primal_cost()[0], rel=1e-12)
+
+
+@pytest.mark.gpu
+def test_gpu_quadratic_tables_match_builtin_path(DD):
+    """h1 = h2 = t^2 through the table path (no shifted gauge) agrees with the
+    built-in quadratic path to the fp32 floor."""
+    from ddinputs import config_images
+    n = 32
+    mu, nu = config_images(1)
+    t = np.arange(n) / n
+    eps = 2.0 / n**2
+    a = DD(mu, nu, eps, 4, err_tol=1e-6)
+    b = DD(mu, nu, eps, 4, err_tol=1e-6)
+    b.set_cost(t**2, t**2)
+    a.iterate(8)
+    b.iterate(8)
+    ca, cb = a.primal_cost()[0], b.primal_cost()[0]
+    assert abs(ca - cb) <= 2e-7 * ca
+    assert np.abs(a.basic_marginals_dense() - b.basic_marginals_dense()).sum() <= 4e-6
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kappa", [2.0])
+def test_gpu_cell_size_16_vs_oracle(DD, kappa):
+    """s = 16 (the paper's cell-size study): composite X cells of
+    32 x 32 px on the SMEM tier; GPU vs oracle sweeps at 64^2."""
+    n, s = 64, 16
+    mu, nu = gaussian_mixture_image(n, 41, 3), gaussian_mixture_image(n, 42, 3)
+    eps = kappa / n**2
+    g = DD(mu, nu, eps, s, err_tol=1e-6)
+    o = Oracle(mu, nu, eps, s, err_tol=1e-6)
+    mass = _mass_i(mu, s)
+    for sweep in range(4):
+        g.iterate(1)
+        o.iterate(1)
+        diff = np.abs(g.basic_marginals_dense() - o.basic_marginals_dense()).sum(1)
+        assert (diff <= 4e-6 * np.maximum(mass, 1e-3)).all(), (sweep, diff.max())
+    cg, co = g.primal_cost()[0], o.primal_cost()[0]
+    assert abs(cg - co) <= 1e-5 * co
+    lx, ly = g.marginal_error()
+    assert lx <= 1e-6 and ly <= 1e-6
+
+
+@pytest.mark.gpu
+def test_gpu_general_cost_box_beyond_capacity_is_enomem(DD):
+    """A general-cost cell whose union box exceeds the SMEM tier is flagged
+    and reported (DD_ENOMEM at dd_synchronize), never solved by the
+    quadratic big-cell path."""
+    import paper_2001_10986_b200 as P
+    n = 256
+    mu, nu = gaussian_mixture_image(n, 5, 3), gaussian_mixture_image(n, 6, 3)
+    t = np.arange(n) / n
+    g = DD(mu, nu, 2.0 / n**2, 8, err_tol=1e-6)
+    g.set_cost(1e-6 * t, 1e-6 * t)          # flat cost: the product coupling's boxes (whole image) stay
+    with pytest.raises(RuntimeError, match="rc="):
+        for _ in range(6):
+            g.iterate(1)
+        g.synchronize()

@@ -55,6 +55,11 @@ extern "C" {
 #define DD_SCHED_LADDER 1  /* multiscale + eps-scaling (A12) */
 
 #define DD_FLAG_DEVICE_INPUT 1u  /* dd_init: mu, nu are device pointers (fp64) */
+#define DD_FLAG_SAFEGUARD 2u     /* eps-raising safeguard (A29): a
+                                    cell whose Sinkhorn hits max_inner_iter or turns non-finite is
+                                    retried from its input alpha at 2^k eps (k = 1, 2, 3; fp64),
+                                    alpha kept and re-solved at eps; CellOut flag 32.
+                                    Cells that still fail are flagged as before (DD_ENOCONV). */
 
 #define DD_PLAN_BASIC_MARGINALS 0
 #define DD_PLAN_COO 1

@@ -530,7 +530,7 @@ static void balance(int nmem, int ny, double** nu_i, const double* target) {
     }
 }
 
-typedef struct { int iters, flag; double err; } cellres_t;
+typedef struct { int iters, flag, safeguard; double err; } cellres_t;
 
 /* Algorithm 2 lines 8-13 for one composite cell J of partition part. */
 static int solve_cell(ddo_ctx* c, int part, int cidx, cellres_t* res) {
@@ -551,8 +551,38 @@ static int solve_cell(ddo_ctx* c, int part, int cidx, cellres_t* res) {
 #ifdef _OPENMP
     nt = c->opt.n_threads > 0 ? c->opt.n_threads : omp_get_max_threads();
 #endif
+    double* f_in = NULL;
+    if (c->opt.safeguard) {
+        f_in = (double*)malloc(sizeof(double) * (size_t)(P.nx > 0 ? P.nx : 1));
+        if (!f_in) { free_prob(&P); return DDO_ENOMEM; }
+        memcpy(f_in, P.f, sizeof(double) * (size_t)P.nx);
+    }
     int src = sinkhorn_dense_k(P.nx, P.ny, P.a, P.b, P.C, c->eps, muJ * c->opt.err_tol,
                                c->opt.max_inner_iter, c->opt.check_every, nt, P.f, P.g, &it, &err);
+    res->safeguard = 0;
+    if (src != DDO_OK && c->opt.safeguard) {
+        /* eps-raising safeguard ("temporarily increasing eps"; S:281 retry at
+         * 2x eps, rescale the potential back, re-solve at the target eps; S:323 at
+         * most 3 attempts; A29): attempt k starts from the cell's input
+         * alpha = f_in - eps log mu at eps_k = 2^k eps, then keeps alpha (the eps
+         * change rule P:1510) and solves at eps; every stage to the same tolerance
+         * and iteration cap. */
+        res->safeguard = 1;
+        for (int k = 1; k <= 3 && src != DDO_OK; ++k) {
+            const double ek = ldexp(c->eps, k);
+            for (int x = 0; x < P.nx; ++x)
+                P.f[x] = (P.a[x] > 0.0) ? f_in[x] - c->eps * log(P.a[x]) + ek * log(P.a[x]) : -INFINITY;
+            int i1 = 0, i2 = 0;
+            sinkhorn_dense_k(P.nx, P.ny, P.a, P.b, P.C, ek, muJ * c->opt.err_tol,
+                             c->opt.max_inner_iter, c->opt.check_every, nt, P.f, P.g, &i1, &err);
+            for (int x = 0; x < P.nx; ++x)
+                if (P.a[x] > 0.0) P.f[x] = P.f[x] - ek * log(P.a[x]) + c->eps * log(P.a[x]);
+            src = sinkhorn_dense_k(P.nx, P.ny, P.a, P.b, P.C, c->eps, muJ * c->opt.err_tol,
+                                   c->opt.max_inner_iter, c->opt.check_every, nt, P.f, P.g, &i2, &err);
+            it += i1 + i2;
+        }
+    }
+    free(f_in);
     res->iters = it; res->err = err; res->flag = src;
     /* line 10: nu_i <- P_Y(pi_cell restricted to X_i x Y) */
     double* nu_i[4];
@@ -634,6 +664,7 @@ static int sweep(ddo_ctx* c) {
         st.iters_sum += res[j].iters;
         if (res[j].iters > st.iters_max) st.iters_max = res[j].iters;
         st.err_x_sum += res[j].err;
+        st.safeguarded += res[j].safeguard;
         if (res[j].flag != DDO_OK) {
             st.failed++;
             if (rc == DDO_OK) rc = res[j].flag;

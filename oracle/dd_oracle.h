@@ -46,6 +46,10 @@ typedef struct {
                               coarse potentials glued (Sec. 6.3) and
                               interpolated linearly in log space onto the fine pixel
                               centres (readings A25, A26); 0 -> cold start alpha = 0 (A14) */
+    int safeguard;         /* 1 -> eps-raising safeguard (A29):
+                              a cell whose Sinkhorn fails (max_inner_iter or non-finite) is
+                              retried from its input alpha at 2^k eps (k = 1, 2, 3), the
+                              result re-solved at eps with alpha kept */
 } ddo_options;
 
 typedef struct {
@@ -53,6 +57,8 @@ typedef struct {
     int iters_max, failed;
     double err_x_sum;
     long long entries;
+    int safeguarded;       /* cells the eps-raising safeguard retried (ddo_options.safeguard) */
+    int pad_;
 } ddo_sweep_stats;
 
 typedef struct {

@@ -107,6 +107,7 @@ int dd_init(shim_ctx** out, int n, const double* mu, const double* nu, int cost,
         c->opt.coarsest_side = opt->coarsest_side;
         c->opt.no_truncate = opt->no_truncate;
         c->opt.check_every = opt->check_every;
+        c->opt.safeguard = (opt->flags & 2u) ? 1 : 0;      /* DD_FLAG_SAFEGUARD */
     }
     c->n = n; c->cell_size = cell_size; c->eps = eps;
     size_t n2 = (size_t)n * n;

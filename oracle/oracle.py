@@ -34,13 +34,14 @@ class _Opt(C.Structure):
                 ("max_inner_iter", C.c_int), ("n_threads", C.c_int),
                 ("schedule", C.c_int), ("eps_start", C.c_double),
                 ("coarsest_side", C.c_int), ("no_truncate", C.c_int), ("empty_init", C.c_int),
-                ("check_every", C.c_int), ("warm_refine", C.c_int)]
+                ("check_every", C.c_int), ("warm_refine", C.c_int), ("safeguard", C.c_int)]
 
 
 class _Stats(C.Structure):
     _fields_ = [("cells", C.c_longlong), ("iters_sum", C.c_longlong),
                 ("iters_max", C.c_int), ("failed", C.c_int),
-                ("err_x_sum", C.c_double), ("entries", C.c_longlong)]
+                ("err_x_sum", C.c_double), ("entries", C.c_longlong),
+                ("safeguarded", C.c_int), ("pad_", C.c_int)]
 
 
 class _Info(C.Structure):
@@ -118,13 +119,14 @@ class Oracle:
 
     def __init__(self, mu, nu, eps, cell_size, *, err_tol=1e-6, trunc_tau=1e-15,
                  max_inner_iter=10000, n_threads=0, schedule=SCHED_FIXED, eps_start=0.0,
-                 coarsest_side=8, no_truncate=False, empty_init=False, check_every=1, warm_refine=False):
+                 coarsest_side=8, no_truncate=False, empty_init=False, check_every=1, warm_refine=False,
+                 safeguard=False):
         self.mu = np.ascontiguousarray(mu, dtype=np.float64)
         self.nu = np.ascontiguousarray(nu, dtype=np.float64)
         n = self.mu.shape[0]
         opt = _Opt(err_tol, trunc_tau, max_inner_iter, n_threads, schedule, eps_start,
                    coarsest_side, 1 if no_truncate else 0, 1 if empty_init else 0, check_every,
-                   1 if warm_refine else 0)
+                   1 if warm_refine else 0, 1 if safeguard else 0)
         self._h = C.c_void_p()
         rc = lib().ddo_init(C.byref(self._h), n, _dp(self.mu), _dp(self.nu), eps, cell_size,
                             C.byref(opt))

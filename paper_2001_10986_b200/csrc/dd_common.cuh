@@ -90,6 +90,7 @@ struct SweepParams {
     const double* h1;
     const double* h2;
     int hst;
+    int safeguard;        // DD_FLAG_SAFEGUARD: eps-raising retry of failing cells (A29)
 };
 
 // ------------------------------------------------------------- helpers --

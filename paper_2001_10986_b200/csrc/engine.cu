@@ -318,6 +318,7 @@ int sweep(dd_ctx* c) {
     cell_rows(c, part, Lr.nb, &p.cr0, &p.cr1);
     p.eps = c->eps;
     p.h1 = c->d_h1; p.h2 = c->d_h2; p.hst = c->L[c->n_layers - 1].side / Lr.side;
+    p.safeguard = (c->opt.flags & DD_FLAG_SAFEGUARD) ? 1 : 0;
     p.kappa = c->eps * (double)Lr.side * (double)Lr.side;
     p.tau = c->tau;
     p.err_tol = c->opt.err_tol;

@@ -1241,11 +1241,14 @@ __device__ int rescue_fp64(const K1Lay& L, const Dims& d, double* F, double* Fn,
 // every output is stored to all replicas (DSMEM); three cluster barriers per
 // iteration.  Rank 0 alone runs the extraction and the epilogue.  gslice is
 // the cluster's (shared) global slice.
-template <int NT, bool BIG, int CS>
+template <int NT, bool BIG, int CS, bool GC>
 __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, unsigned char* gslice) {
     static_assert(CS == 1 || BIG, "cluster tier = big-cell path");
-    // general costs (dd_set_cost) run on the SMEM tier only
-    const bool gc = !BIG && p.h1 != nullptr;
+    static_assert(!(GC && BIG), "general costs run on the SMEM tier only");
+    // general costs (dd_set_cost) run on the SMEM tier only (DESIGN.md "general
+    // costs"): a separate kernel instantiation, so the quadratic kernels carry no
+    // general-cost code
+    constexpr bool gc = GC;
     const K1Lay L = k1_carve(base, p.s, p.bcap, BIG, NT / 32, gc);
     const int rank = CS > 1 ? (int)cluster_rank() : 0;
     __shared__ int4 s_box[4];
@@ -1511,6 +1514,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     double err = 0.0;
     double err_ck = INFINITY;       // X-error at the last stall checkpoint
     bool rescue = false;
+    bool safeguard = false;     // eps-raising safeguard (DD_FLAG_SAFEGUARD, A29)
     PROF_T(t_loop0);
     while (true) {
         const bool exact = (it == 0);
@@ -1555,7 +1559,11 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         PROF_ADD(4, tf - te); PROF_ADD(5, tg - tf);
         ++it;
         if (err <= tol && it % p.check_every == 0) break;
-        if (it >= p.max_iter || !(err == err)) { co.flags |= 1; break; }
+        if (it >= p.max_iter || !(err == err)) {
+            if (p.safeguard) safeguard = true;
+            else co.flags |= 1;
+            break;
+        }
         // stall at the fp32 error floor: < 2 % progress over 256 iterations
         // within 1.5x of the tolerance -> continue in fp64 (rescue_fp64)
         if ((it & 255) == 0) {
@@ -1563,6 +1571,11 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
             err_ck = err;
         }
         float2* t = Fc; Fc = Fn; Fn = t;
+    }
+    if (CS == 1 && p.safeguard) {
+        // non-finite potentials (nu_cell(y) > 0 unreachable) also
+        // trigger the safeguard; the retry recomputes them
+        if (__syncthreads_or(nonfinite)) { safeguard = true; nonfinite = 0; }
     }
     PROF_T(t_loop1);
     PROF_ADD(6, t_loop1 - t_loop0);
@@ -1580,11 +1593,11 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         if (rank != 0) return;
         peer_fallbacks = L.WK[3];
     }
-    if (rescue) {
+    if (rescue || safeguard) {
         // fp64 continuation (rescue_fp64): potentials and Y-side arrays as fp64
         double* F64 = reinterpret_cast<double*>(Fc);
         double* Fn64 = reinterpret_cast<double*>(Fn);
-        for (int x = tid; x < nx; x += NT) {
+        for (int x = tid; rescue && x < nx; x += NT) {
             const int i = (x / d.ac) * d.pX + x % d.ac;
             const float2 f = Fc[i];
             F64[i] = f.x == -INFINITY ? -INFINITY : join_hl(f);
@@ -1611,12 +1624,59 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         // few hundred (measured 257); a cell that is merely this slow in fp64
         // too (the oracle needs > 4e4 iterations on such cells) keeps its
         // Y-feasible plan and is flagged (reading A6)
-        const int n = rescue_fp64<NT>(L, d, F64, Fn64, G64, str, LNU64, str, cf, tol,
-                                      max(1, min(kRescueIters, p.max_iter - it)), e64);
-        it += n;
-        err = e64;
-        co.flags |= 16;                       // solved to the tolerance by the fp64 rescue
-        if (!(err <= tol)) co.flags |= 1;
+        if (rescue) {
+            const int n = rescue_fp64<NT>(L, d, F64, Fn64, G64, str, LNU64, str, cf, tol,
+                                          max(1, min(kRescueIters, p.max_iter - it)), e64);
+            it += n;
+            err = e64;
+            co.flags |= 16;                   // solved to the tolerance by the fp64 rescue
+            if (!(err <= tol)) {
+                if (p.safeguard) safeguard = true;
+                else co.flags |= 1;
+            }
+        }
+        if (safeguard) {
+            // eps-raising safeguard ("temporarily increasing eps"; S:281,
+            // S:323; A29): attempt k restarts from the cell's INPUT
+            // alpha at eps_k = 2^k eps (absorbed F' = r (F0 - log mu) + log mu,
+            // r = 2^-k, costs r C: alpha kept), then re-solves at eps
+            // from the result, every stage to the same tolerance and cap
+            bool ok = false;
+            for (int k = 1; k <= 3 && !ok; ++k) {
+                const double r = ldexp(1.0, -k);
+                for (int x = tid; x < nx; x += NT) {
+                    int xr, xc;
+                    goff(x / d.ac, x % d.ac, xr, xc);
+                    const long long g = (long long)(R0 + xr) * p.side + (C0 + xc);
+                    double f = -INFINITY;
+                    if (p.mu[g] > 0.0) {
+                        const double sh = gc ? 0.0 : ((2.0 * xr + Dr) * Dr + (2.0 * xc + Dc) * Dc) * inv_kappa;
+                        const double F0 = p.alpha[g] * inv_eps + p.logmu[g] - sh - lambda;
+                        f = r * (F0 - p.logmu[g]) + p.logmu[g];
+                    }
+                    F64[(x / d.ac) * d.pX + x % d.ac] = f;
+                }
+                __syncthreads();
+                CostF ck = cf;
+                ck.ik *= r;
+                ck.ie *= r;
+                double e1 = INFINITY;
+                it += rescue_fp64<NT>(L, d, F64, Fn64, G64, str, LNU64, str, ck, tol, p.max_iter, e1);
+                for (int x = tid; x < nx; x += NT) {
+                    int xr, xc;
+                    goff(x / d.ac, x % d.ac, xr, xc);
+                    const long long g = (long long)(R0 + xr) * p.side + (C0 + xc);
+                    const int i = (x / d.ac) * d.pX + x % d.ac;
+                    if (F64[i] > -INFINITY) F64[i] = (F64[i] - p.logmu[g]) / r + p.logmu[g];
+                }
+                __syncthreads();
+                it += rescue_fp64<NT>(L, d, F64, Fn64, G64, str, LNU64, str, cf, tol, p.max_iter, e64);
+                ok = e64 <= tol;
+            }
+            err = e64;
+            co.flags |= 32;
+            if (!ok) co.flags |= 1;
+        }
         for (int x = tid; x < nx; x += NT) {
             const int i = (x / d.ac) * d.pX + x % d.ac;
             const double f = F64[i];
@@ -1803,7 +1863,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
 // BIG = true: fused Y2+X1 path, O(a b) SMEM + a global slice per CTA;
 // CS > 1: persistent clusters of CS CTAs, one cell per cluster at a time,
 // one global slice per cluster.
-template <int NT, bool BIG, int MINB, int CS>
+template <int NT, bool BIG, int MINB, int CS, bool GC>
 __global__ void __launch_bounds__(NT, MINB) k1_cell_solve(SweepParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_cell;
@@ -1823,7 +1883,7 @@ __global__ void __launch_bounds__(NT, MINB) k1_cell_solve(SweepParams p) {
             __syncthreads();
             const int cell = s_cell;
             if (cell < 0) return;
-            solve_cell<NT, BIG, 1>(p, cell, base, gslice);
+            solve_cell<NT, BIG, 1, GC>(p, cell, base, gslice);
             __syncthreads();
         }
     } else {
@@ -1840,7 +1900,7 @@ __global__ void __launch_bounds__(NT, MINB) k1_cell_solve(SweepParams p) {
             cluster_sync_all();
             const int cell = s_cell;
             if (cell < 0) return;        // all CTAs of the cluster leave together
-            solve_cell<NT, BIG, CS>(p, cell, base, gslice);
+            solve_cell<NT, BIG, CS, false>(p, cell, base, gslice);
             cluster_sync_all();          // rank 0's epilogue done before the next cell's stores
         }
     }
@@ -1977,7 +2037,7 @@ cudaError_t launch_k0(const SweepParams& p, int b0, int b1, int* lists, int* cou
     return cudaGetLastError();
 }
 
-template <int NT, bool BIG, int MINB, int CS>
+template <int NT, bool BIG, int MINB, int CS, bool GC = false>
 static cudaError_t launch_tier(const SweepParams& p, int grid, size_t smem, cudaStream_t st) {
     // the SMEM opt-in is a per-device function attribute: cache it per device
     static size_t attr[64] = {0};
@@ -1988,14 +2048,14 @@ static cudaError_t launch_tier(const SweepParams& p, int grid, size_t smem, cuda
     // opt in whenever the request grows: the 48 KB default covers static +
     // dynamic SMEM together, so a dynamic size just under 48 KB can fail too
     if (smem > attr[dev]) {
-        e = cudaFuncSetAttribute(k1_cell_solve<NT, BIG, MINB, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = cudaFuncSetAttribute(k1_cell_solve<NT, BIG, MINB, CS, GC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr[dev] = smem;
     }
     SweepParams q = p;
     q.smem_bytes = smem;
     if constexpr (CS == 1) {
-        k1_cell_solve<NT, BIG, MINB, CS><<<grid, NT, smem, st>>>(q);
+        k1_cell_solve<NT, BIG, MINB, CS, GC><<<grid, NT, smem, st>>>(q);
         return cudaGetLastError();
     } else {
         cudaLaunchConfig_t cfg = {};
@@ -2010,7 +2070,7 @@ static cudaError_t launch_tier(const SweepParams& p, int grid, size_t smem, cuda
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        return cudaLaunchKernelEx(&cfg, k1_cell_solve<NT, BIG, MINB, CS>, q);
+        return cudaLaunchKernelEx(&cfg, k1_cell_solve<NT, BIG, MINB, CS, GC>, q);
     }
 }
 
@@ -2018,7 +2078,10 @@ static cudaError_t launch_tier(const SweepParams& p, int grid, size_t smem, cuda
 // tier 1: BIG path, 256 threads, 3 CTAs/SM; tier 2: BIG path, 768 threads, 1 CTA/SM (both <= 80 registers);
 // tier 3 (cluster tier): tier 2's CTA in clusters of kClusterSize, grid = number of clusters.
 cudaError_t launch_k1(const SweepParams& p, int tier, int grid, size_t smem, cudaStream_t st) {
-    if (tier == 0) return launch_tier<256, false, DD_T0_MINB, 1>(p, grid, smem, st);
+    if (tier == 0) {
+        if (p.h1) return launch_tier<256, false, DD_T0_MINB, 1, true>(p, grid, smem, st);
+        return launch_tier<256, false, DD_T0_MINB, 1>(p, grid, smem, st);
+    }
     if (tier == 1) return launch_tier<kT1Threads, true, kT1PerSM, 1>(p, grid, smem, st);
     if (tier == 2) return launch_tier<kT2Threads, true, 1, 1>(p, grid, smem, st);
     return launch_tier<kT2Threads, true, 1, kClusterSize>(p, grid, smem, st);
@@ -2037,13 +2100,13 @@ int k1_max_clusters(size_t smem) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (cudaFuncSetAttribute(k1_cell_solve<kT2Threads, true, 1, kClusterSize>,
+    if (cudaFuncSetAttribute(k1_cell_solve<kT2Threads, true, 1, kClusterSize, false>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, k1_cell_solve<kT2Threads, true, 1, kClusterSize>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&n, k1_cell_solve<kT2Threads, true, 1, kClusterSize, false>, &cfg) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }

@@ -18,6 +18,7 @@ OK, EINVAL, ENOCONV, ENUMERIC, ECUDA, ENCCL, ENOMEM = 0, 1, 2, 3, 4, 5, 6
 COST_SQEUCLID = 0
 SCHED_FIXED, SCHED_LADDER = 0, 1
 FLAG_DEVICE_INPUT = 1
+FLAG_SAFEGUARD = 2
 PLAN_BASIC_MARGINALS, PLAN_COO = 0, 1
 
 # every symbol include/dd.h declares (checked by tests/test_abi.py)
@@ -149,7 +150,7 @@ class DD:
                  max_inner_iter=10000, schedule=SCHED_FIXED, eps_start=0.0, coarsest_side=8,
                  no_truncate=False, device=0, pool_capacity=0, stream=None, device_input=False,
                  bcap_main=0, bcap_big=0, cold_refine=False, check_every=1, cluster=0,
-                 cluster_theta=0, n_clusters=0):
+                 cluster_theta=0, n_clusters=0, safeguard=False):
         opt = Options()
         opt.err_tol = err_tol
         opt.trunc_tau = trunc_tau
@@ -168,10 +169,11 @@ class DD:
         opt.reserved[3] = cluster            # K1 cluster tier: 0 off, 2 auto (long poles), 1 every big-path cell
         opt.reserved[4] = cluster_theta      # routing threshold in % (0 -> default)
         opt.reserved[5] = n_clusters         # persistent clusters (0 -> default)
+        opt.flags = FLAG_SAFEGUARD if safeguard else 0
         self._h = C.c_void_p()
         if device_input:
             # mu, nu: objects exposing data_ptr() (device fp64) and a square shape
-            opt.flags = FLAG_DEVICE_INPUT
+            opt.flags |= FLAG_DEVICE_INPUT
             n = int(mu.shape[0])
             pm, pn = C.c_void_p(mu.data_ptr()), C.c_void_p(nu.data_ptr())
             self._keep = (mu, nu)

@@ -98,7 +98,10 @@ typedef struct {                /* zero-initialised fields take the defaults */
                                    [4] > 0: cluster routing threshold theta in % (default 300:
                                    predicted work >= theta * sweep work / #SMs);
                                    [5] > 0: persistent clusters (default 6, capped by
-                                   cudaOccupancyMaxActiveClusters) */
+                                   cudaOccupancyMaxActiveClusters);
+                                   [6] > 0: testing: box-side cap of the on-chip tiers; larger
+                                   cells run on tier G (the SMEM-tier kernel on global-memory
+                                   layouts, which serves boxes of any size) */
 } dd_options;
 
 typedef struct {                /* one sweep (or accumulated totals) */

@@ -53,7 +53,7 @@ cudaError_t launch_k1(const SweepParams& p, int tier, int grid, size_t smem, cud
 int k1_max_clusters(size_t smem);
 cudaError_t launch_k0_cluster(const int* sorted, int* counts, int ncap, const int* bside, float theta, int nsm,
                               int mode, int* list3, cudaStream_t st);
-cudaError_t launch_k0(const SweepParams& p, int b0, int b1, int* lists, int* counts, int ncap, int* bside,
+cudaError_t launch_k0(const SweepParams& p, int b0, int b1, int b2, int* lists, int* counts, int ncap, int* bside,
                       int* sorted, cudaStream_t st);
 cudaError_t launch_slab_export(const int4* box, const long long* off, const double* pool, int n, void* slab,
                                long long cap_bytes, long long* scratch, int* flag, cudaStream_t st);

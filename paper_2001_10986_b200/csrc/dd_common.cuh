@@ -91,6 +91,11 @@ struct SweepParams {
     const double* h2;
     int hst;
     int safeguard;        // DD_FLAG_SAFEGUARD: eps-raising retry of failing cells (A29)
+    // tier G (SMEM-tier kernel on a global-memory layout): the
+    // cells beyond the largest on-chip tier; CTA b carves its K1Lay from
+    // gbase + b * gbase_bytes instead of shared memory
+    unsigned char* gbase;
+    long long gbase_bytes;
 };
 
 // ------------------------------------------------------------- helpers --

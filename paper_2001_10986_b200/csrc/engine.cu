@@ -106,6 +106,12 @@ struct dd_ctx {
     // general separable cost (dd_set_cost): finest-grid tables h1 (rows), h2 (columns)
     double* d_h1 = nullptr;
     double* d_h2 = nullptr;
+    // tier G: per-CTA global-memory layouts of the SMEM-tier kernel
+    // for the cells beyond every on-chip tier (allocated at the first layer
+    // whose boxes can exceed the on-chip caps)
+    unsigned char* gslab = nullptr;
+    long long gslab_bytes = 0;
+    size_t gslab_alloc = 0;
     bool serial = false;            // DD_SERIAL_TIERS=1: all K1 tiers on one stream (profiling)
     long long xoff_n = 0;
     // host bookkeeping
@@ -246,7 +252,8 @@ constexpr int kCap1 = DD_T1_CAP, kCap2 = 704;
 #ifndef DD_NCL
 #define DD_NCL 6
 #endif
-constexpr int kDefaultClusters = DD_NCL;   // persistent clusters of the cluster tier   // tier-1 cap: measured best split
+constexpr int kDefaultClusters = DD_NCL;   // persistent clusters of the cluster tier
+constexpr int kTierG = 4;                  // CTAs of tier G (global-memory layouts)
 // SMEM per CTA: 228 KB per SM shared by the resident CTAs, 1 KB reserved per CTA, ~1 KB static
 constexpr size_t kSmem1 = 233472 / kT1PerSM - 2048, kSmem2 = 220 * 1024;
 void tier_caps(int s, int opt_main, int opt_big, int* b0, int* b1, int* b2) {
@@ -286,6 +293,11 @@ void choose_caps(dd_ctx* c, int s) {
     c->bcap_big = std::min(b1, c->slice_cap[0]);
     c->smem_big = k1_smem_bytes_host(s, c->bcap_big, true, kT1Threads / 32);
     c->bcap_big2 = std::min(b2, c->slice_cap[1]);
+    if (c->opt.reserved[6] > 0) {     // testing: cells above this side go to tier G
+        c->bcap_big2 = std::max(std::min(c->bcap_big2, c->opt.reserved[6]), c->bcap_main);
+        c->bcap_big = std::min(c->bcap_big, c->bcap_big2);
+        c->smem_big = k1_smem_bytes_host(s, c->bcap_big, true, kT1Threads / 32);
+    }
     c->smem_big2 = k1_smem_bytes_host(s, c->bcap_big2, true, kT2Threads / 32);
 }
 
@@ -311,7 +323,7 @@ int sweep(dd_ctx* c) {
     choose_caps(c, Lr.s);
     CK(cudaMemsetAsync(c->bump, 0, sizeof(unsigned long long), c->st));
     CK(cudaMemsetAsync(c->counters, 0, 6 * sizeof(int), c->st));
-    CK(cudaMemsetAsync(c->counters + 8, 0, 4 * sizeof(int), c->st));
+    CK(cudaMemsetAsync(c->counters + 8, 0, 6 * sizeof(int), c->st));
     SweepParams p{};
     p.part = part;
     p.side = Lr.side; p.s = Lr.s; p.nb = Lr.nb; p.nca = nca; p.ncells = ncells;
@@ -342,7 +354,8 @@ int sweep(dd_ctx* c) {
     if (rc) return rc;
     CK(cudaEventRecord(ev.e[0], c->st));
     int* sorted = c->lists + 3 * (size_t)c->ncell_max;
-    CK(launch_k0(p, c->bcap_main, c->bcap_big, c->lists, c->counters, c->ncell_max, c->bside, sorted, c->st));
+    CK(launch_k0(p, c->bcap_main, c->bcap_big, c->bcap_big2, c->lists, c->counters, c->ncell_max, c->bside, sorted,
+                 c->st));
     int* list3 = c->lists + 5 * (size_t)c->ncell_max;
     if (c->ncl > 0)
         CK(launch_k0_cluster(sorted, c->counters, c->ncell_max, c->bside, c->cl_theta, c->nsm, c->cl_mode, list3,
@@ -392,6 +405,29 @@ int sweep(dd_ctx* c) {
         q.list_in = c->lists; q.n_in = c->counters; q.work_counter = c->counters + 3;
         CK(launch_k1(q, 0, std::min(ncells, c->grid_big * 8), c->smem_main, c->st));
     }
+    bool tier_g = false;
+    if (Lr.side > c->bcap_big2) {
+        // tier G: cells whose union box exceeds every on-chip tier (K0 list 6)
+        // run the SMEM-tier kernel on a global-memory layout, kTierG CTAs
+        const bool gc = c->d_h1 != nullptr;
+        const long long per = (long long)((k1_smem_bytes_host(Lr.s, Lr.side, false, 0, gc) + 255) & ~size_t(255));
+        const size_t need = (size_t)per * kTierG;
+        if (need > c->gslab_alloc) {
+            CK(cudaStreamSynchronize(c->st));
+            if (c->gslab) CK(cudaFree(c->gslab));
+            c->gslab = nullptr;
+            c->gslab_alloc = 0;
+            CK(cudaMalloc(&c->gslab, need));
+            c->gslab_alloc = need;
+        }
+        SweepParams q = p;
+        q.bcap = Lr.side;
+        q.list_in = c->lists + 6 * (size_t)c->ncell_max; q.n_in = c->counters + 12; q.work_counter = c->counters + 13;
+        q.gbase = c->gslab; q.gbase_bytes = per;
+        q.poison = 0;
+        CK(launch_k1(q, 0, kTierG, 0, c->st));
+        tier_g = true;
+    }
     CK(cudaEventRecord(c->ev_join[0], c->st_t[0]));
     CK(cudaEventRecord(c->ev_join[1], c->st_t[1]));
     CK(cudaStreamWaitEvent(c->st, c->ev_join[0], 0));
@@ -411,7 +447,7 @@ int sweep(dd_ctx* c) {
                            c->counters + 6, c->counters + 2, c->st));
     CK(cudaEventRecord(ev.e[2], c->st));
     c->pending.push_back(ev);
-    c->launches_pending += c->ncl > 0 ? 10 : 8;
+    c->launches_pending += (c->ncl > 0 ? 10 : 8) + (tier_g ? 1 : 0);
     c->half_index++;
     c->last_part = part;
     if (c->pending.size() > 512) return harvest(c);
@@ -442,7 +478,7 @@ void free_all(dd_ctx* c) {
     void* ptrs[] = {c->alphaA, c->alphaB, c->box, c->box2, c->off, c->off2, c->pool, c->scratch,
                     c->bump, c->lists, c->bside, c->ipred, c->slices[0], c->slices[1], c->counters, c->cellout, c->d_total, c->d_last, c->d_tot,
                     c->eval_scratch, c->eval_res, c->d_sums, c->yacc, c->partial, c->d_xoff, c->glue, c->cl_slices,
-                    c->d_h1, c->d_h2};
+                    c->d_h1, c->d_h2, c->gslab};
     for (void* q : ptrs) if (q) cudaFree(q);
     for (auto& ev : c->pending) for (int k = 0; k < 3; ++k) cudaEventDestroy(ev.e[k]);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -724,7 +760,7 @@ int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, d
     CK(cudaMalloc(&c->scratch, (size_t)c->cap * sizeof(double)));
     CK(cudaMalloc(&c->bump, sizeof(unsigned long long)));
     c->ncell_max = (nbmax / 2 + 1) * (nbmax / 2 + 1);
-    CK(cudaMalloc(&c->lists, (size_t)6 * c->ncell_max * sizeof(int)));
+    CK(cudaMalloc(&c->lists, (size_t)7 * c->ncell_max * sizeof(int)));
     CK(cudaMalloc(&c->bside, (size_t)c->ncell_max * sizeof(int)));
     CK(cudaMalloc(&c->ipred, (size_t)2 * c->ncell_max * sizeof(int)));
     CK(cudaMalloc(&c->counters, 16 * sizeof(int)));

@@ -959,13 +959,15 @@ __device__ __forceinline__ void x2_out(const K1Lay& L, const Dims& d, const Grid
                                        float2 lm0, float2 lm1, float2 fo0, float2 fo1, float S0, float S1,
                                        float2 a, const float2* __restrict__ Ur, float2* Fout,
                                        int& fallbacks, int& nonfinite);
-template <int NT, int CS>
+// P threads per task (x1 pair, x2) split the y1 range in P fixed halves.  P is
+// a function of the CELL (its row count), never of the CTA shape, so every
+// tier gives the same bits: P = 2 for br <= kX2Wide (tier 1's cells), P = 4
+// above (the tier-2 cells: 512 of 768 threads busy instead of 256; in tier 1
+// such a cell takes two task rounds of the same per-thread work).
+constexpr int kX2Wide = 120;
+template <int NT, int CS, int P>
 __device__ void x2_finalize(const K1Lay& L, const Dims& d, const Grid& gq, const float2* Fcur, float2* Fout,
                             int& fallbacks, int& nonfinite) {
-#ifndef DD_X2P
-#define DD_X2P 2
-#endif
-    constexpr int P = DD_X2P;
     constexpr int SLOTS = NT / P;          // task slots per CTA
     static_assert(NT % (32 * P) == 0 && (P == 2 || P == 4), "x2 split");
     const int rank = CS > 1 ? (int)cluster_rank() : 0;
@@ -1539,7 +1541,8 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         cta_or_cluster_sync<CS>();
         PROF_T(te);
         if (BIG) {
-            x2_finalize<NT, CS>(L, d, gq, Fc, Fn, fallbacks, nonfinite);
+            if (d.br > kX2Wide) x2_finalize<NT, CS, 4>(L, d, gq, Fc, Fn, fallbacks, nonfinite);
+            else x2_finalize<NT, CS, 2>(L, d, gq, Fc, Fn, fallbacks, nonfinite);
         } else {
             if (gc) lse_pass<PX2, NT, true>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
             else lse_pass<PX2, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
@@ -1868,6 +1871,7 @@ __global__ void __launch_bounds__(NT, MINB) k1_cell_solve(SweepParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_cell;
     unsigned char* base = smem;
+    if (!BIG && p.gbase) base = p.gbase + (long long)blockIdx.x * p.gbase_bytes;   // tier G
     const int slot = CS > 1 ? blockIdx.x / CS : blockIdx.x;
     unsigned char* gslice = BIG ? p.gscratch + (long long)slot * p.gslice : nullptr;
     if (p.poison) {     // testing: SMEM the path did not write reads as NaN
@@ -1910,7 +1914,7 @@ __global__ void __launch_bounds__(NT, MINB) k1_cell_solve(SweepParams p) {
 // (tier 0 <= b0: SMEM path; tier 1 <= b1 and tier 2 (beyond): BIG path;
 // cells beyond tier 2's capacity are flagged by the solve), and record the
 // side for the LPT ordering of the big tiers.
-__global__ void k0_classify(SweepParams p, int b0, int b1, int* lists, int* counts, int ncap, int* bside,
+__global__ void k0_classify(SweepParams p, int b0, int b1, int b2, int* lists, int* counts, int ncap, int* bside,
                             unsigned long long* wsum) {
     const int cell = blockIdx.x * blockDim.x + threadIdx.x;
     if (cell >= p.ncells) return;
@@ -1935,9 +1939,10 @@ __global__ void k0_classify(SweepParams p, int b0, int b1, int* lists, int* coun
         }
     const int bmax = y1 >= 0 ? max(y1 - y0 + 1, x1 - x0 + 1) : 0;
     const bool small_x = p.s < 4;       // the BIG path needs a_c % 4 == 0
-    const int tier = (bmax <= b0 || small_x) ? 0 : (bmax <= b1 ? 1 : 2);
-    const int k = atomicAdd(&counts[tier], 1);
-    lists[tier * ncap + k] = cell;
+    const int tier = bmax <= b0 ? 0 : small_x ? 3 : (bmax <= b1 ? 1 : (bmax <= b2 ? 2 : 3));
+    // tier 3 here = tier G (beyond every on-chip tier): list 6, count counts[12]
+    const int k = atomicAdd(&counts[tier == 3 ? 12 : tier], 1);
+    lists[(tier == 3 ? 6 : tier) * ncap + k] = cell;
     // LPT key ~ predicted solve time: box area x the cell's iteration count in
     // this partition's previous sweep (1 before the first), log-binned
     const int ip = p.ipred ? max(1, p.ipred[cell]) : 1;
@@ -2027,9 +2032,9 @@ cudaError_t launch_k0_cluster(const int* sorted, int* counts, int ncap, const in
 
 size_t k1_smem_bytes_host(int s, int bcap, bool big, int nwarps, bool gc) { return k1_smem_bytes(s, bcap, big, nwarps, gc); }
 
-cudaError_t launch_k0(const SweepParams& p, int b0, int b1, int* lists, int* counts, int ncap, int* bside,
+cudaError_t launch_k0(const SweepParams& p, int b0, int b1, int b2, int* lists, int* counts, int ncap, int* bside,
                       int* sorted, cudaStream_t st) {
-    k0_classify<<<(p.ncells + 255) / 256, 256, 0, st>>>(p, b0, b1, lists, counts, ncap, bside,
+    k0_classify<<<(p.ncells + 255) / 256, 256, 0, st>>>(p, b0, b1, b2, lists, counts, ncap, bside,
                                                          reinterpret_cast<unsigned long long*>(counts + 10));
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -150,7 +150,7 @@ class DD:
                  max_inner_iter=10000, schedule=SCHED_FIXED, eps_start=0.0, coarsest_side=8,
                  no_truncate=False, device=0, pool_capacity=0, stream=None, device_input=False,
                  bcap_main=0, bcap_big=0, cold_refine=False, check_every=1, cluster=0,
-                 cluster_theta=0, n_clusters=0, safeguard=False):
+                 cluster_theta=0, n_clusters=0, safeguard=False, bcap_onchip=0):
         opt = Options()
         opt.err_tol = err_tol
         opt.trunc_tau = trunc_tau
@@ -169,6 +169,7 @@ class DD:
         opt.reserved[3] = cluster            # K1 cluster tier: 0 off, 2 auto (long poles), 1 every big-path cell
         opt.reserved[4] = cluster_theta      # routing threshold in % (0 -> default)
         opt.reserved[5] = n_clusters         # persistent clusters (0 -> default)
+        opt.reserved[6] = bcap_onchip        # testing: larger boxes -> tier G (global-memory layouts)
         opt.flags = FLAG_SAFEGUARD if safeguard else 0
         self._h = C.c_void_p()
         if device_input:

@@ -959,13 +959,15 @@ __device__ __forceinline__ void x2_out(const K1Lay& L, const Dims& d, const Grid
                                        float2 lm0, float2 lm1, float2 fo0, float2 fo1, float S0, float S1,
                                        float2 a, const float2* __restrict__ Ur, float2* Fout,
                                        int& fallbacks, int& nonfinite);
-// P threads per task (x1 pair, x2) split the y1 range in P fixed halves.  P is
-// a function of the CELL (its row count), never of the CTA shape, so every
-// tier gives the same bits: P = 2 for br <= kX2Wide (tier 1's cells), P = 4
-// above (the tier-2 cells: 512 of 768 threads busy instead of 256; in tier 1
-// such a cell takes two task rounds of the same per-thread work).
-constexpr int kX2Wide = 120;
-template <int NT, int CS, int P>
+// P threads per task (x1 pair, x2) split the y1 range in P fixed parts.  P is
+// a constant (never the CTA shape), so every tier gives the same bits.
+// Measured (profiles/r02/ab_x2_p4.log): P = 4 for the tier-2 cells (b_r > 120,
+// 512 of 768 threads busy instead of 256) was 1.3-1.7 % SLOWER on cfg 5 than
+// P = 2 everywhere, and P = 4 in tier 1 (two task rounds) 4 % slower.
+#ifndef DD_X2P
+#define DD_X2P 2
+#endif
+template <int NT, int CS, int P = DD_X2P>
 __device__ void x2_finalize(const K1Lay& L, const Dims& d, const Grid& gq, const float2* Fcur, float2* Fout,
                             int& fallbacks, int& nonfinite) {
     constexpr int SLOTS = NT / P;          // task slots per CTA
@@ -1541,8 +1543,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         cta_or_cluster_sync<CS>();
         PROF_T(te);
         if (BIG) {
-            if (d.br > kX2Wide) x2_finalize<NT, CS, 4>(L, d, gq, Fc, Fn, fallbacks, nonfinite);
-            else x2_finalize<NT, CS, 2>(L, d, gq, Fc, Fn, fallbacks, nonfinite);
+            x2_finalize<NT, CS>(L, d, gq, Fc, Fn, fallbacks, nonfinite);
         } else {
             if (gc) lse_pass<PX2, NT, true>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
             else lse_pass<PX2, NT>(L, d, gq, exact, Fc, Fn, e_loc, fallbacks, nonfinite);
@@ -1866,12 +1867,14 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
 // BIG = true: fused Y2+X1 path, O(a b) SMEM + a global slice per CTA;
 // CS > 1: persistent clusters of CS CTAs, one cell per cluster at a time,
 // one global slice per cluster.
-template <int NT, bool BIG, int MINB, int CS, bool GC>
+template <int NT, bool BIG, int MINB, int CS, bool GC, bool GM>
 __global__ void __launch_bounds__(NT, MINB) k1_cell_solve(SweepParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_cell;
-    unsigned char* base = smem;
-    if (!BIG && p.gbase) base = p.gbase + (long long)blockIdx.x * p.gbase_bytes;   // tier G
+    // GM (tier G): the layout in a per-CTA global slice; otherwise shared
+    // memory (a separate instantiation, so the on-chip tiers keep shared-window
+    // addressing for every K1Lay array)
+    unsigned char* base = GM ? p.gbase + (long long)blockIdx.x * p.gbase_bytes : smem;
     const int slot = CS > 1 ? blockIdx.x / CS : blockIdx.x;
     unsigned char* gslice = BIG ? p.gscratch + (long long)slot * p.gslice : nullptr;
     if (p.poison) {     // testing: SMEM the path did not write reads as NaN
@@ -2042,7 +2045,7 @@ cudaError_t launch_k0(const SweepParams& p, int b0, int b1, int b2, int* lists, 
     return cudaGetLastError();
 }
 
-template <int NT, bool BIG, int MINB, int CS, bool GC = false>
+template <int NT, bool BIG, int MINB, int CS, bool GC = false, bool GM = false>
 static cudaError_t launch_tier(const SweepParams& p, int grid, size_t smem, cudaStream_t st) {
     // the SMEM opt-in is a per-device function attribute: cache it per device
     static size_t attr[64] = {0};
@@ -2053,14 +2056,14 @@ static cudaError_t launch_tier(const SweepParams& p, int grid, size_t smem, cuda
     // opt in whenever the request grows: the 48 KB default covers static +
     // dynamic SMEM together, so a dynamic size just under 48 KB can fail too
     if (smem > attr[dev]) {
-        e = cudaFuncSetAttribute(k1_cell_solve<NT, BIG, MINB, CS, GC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = cudaFuncSetAttribute(k1_cell_solve<NT, BIG, MINB, CS, GC, GM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr[dev] = smem;
     }
     SweepParams q = p;
     q.smem_bytes = smem;
     if constexpr (CS == 1) {
-        k1_cell_solve<NT, BIG, MINB, CS, GC><<<grid, NT, smem, st>>>(q);
+        k1_cell_solve<NT, BIG, MINB, CS, GC, GM><<<grid, NT, smem, st>>>(q);
         return cudaGetLastError();
     } else {
         cudaLaunchConfig_t cfg = {};
@@ -2075,7 +2078,7 @@ static cudaError_t launch_tier(const SweepParams& p, int grid, size_t smem, cuda
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        return cudaLaunchKernelEx(&cfg, k1_cell_solve<NT, BIG, MINB, CS, GC>, q);
+        return cudaLaunchKernelEx(&cfg, k1_cell_solve<NT, BIG, MINB, CS, GC, GM>, q);
     }
 }
 
@@ -2084,6 +2087,10 @@ static cudaError_t launch_tier(const SweepParams& p, int grid, size_t smem, cuda
 // tier 3 (cluster tier): tier 2's CTA in clusters of kClusterSize, grid = number of clusters.
 cudaError_t launch_k1(const SweepParams& p, int tier, int grid, size_t smem, cudaStream_t st) {
     if (tier == 0) {
+        if (p.gbase) {          // tier G: the SMEM-tier kernel on global-memory layouts
+            if (p.h1) return launch_tier<256, false, DD_T0_MINB, 1, true, true>(p, grid, 0, st);
+            return launch_tier<256, false, DD_T0_MINB, 1, false, true>(p, grid, 0, st);
+        }
         if (p.h1) return launch_tier<256, false, DD_T0_MINB, 1, true>(p, grid, smem, st);
         return launch_tier<256, false, DD_T0_MINB, 1>(p, grid, smem, st);
     }
@@ -2105,13 +2112,13 @@ int k1_max_clusters(size_t smem) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (cudaFuncSetAttribute(k1_cell_solve<kT2Threads, true, 1, kClusterSize, false>,
+    if (cudaFuncSetAttribute(k1_cell_solve<kT2Threads, true, 1, kClusterSize, false, false>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, k1_cell_solve<kT2Threads, true, 1, kClusterSize, false>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&n, k1_cell_solve<kT2Threads, true, 1, kClusterSize, false, false>, &cfg) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }

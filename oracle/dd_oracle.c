@@ -291,14 +291,15 @@ int ddo_init(ddo_ctx** out, int n, const double* mu, const double* nu, double ep
     }
     if (!(eps > 0.0) || !isfinite(eps)) { set_err(c, "eps must be > 0"); return DDO_EINVAL; }
     if (!mu || !nu) { set_err(c, "null marginal"); return DDO_EINVAL; }
-    double smu = 0, snu = 0;
+    ksum_t ksm = {0, 0}, ksn = {0, 0};      /* compensated (A17): input validation only */
     for (size_t k = 0; k < (size_t)n * n; ++k) {
         if (!isfinite(mu[k]) || mu[k] < 0 || !isfinite(nu[k]) || nu[k] < 0) {
             set_err(c, "marginals must be finite and >= 0 (index %zu)", k);
             return DDO_EINVAL;
         }
-        smu += mu[k]; snu += nu[k];
+        ks_add(&ksm, mu[k]); ks_add(&ksn, nu[k]);
     }
+    double smu = ks_get(&ksm), snu = ks_get(&ksn);
     if (!(smu > 0) || fabs(smu - snu) > 1e-12 * smu) {
         set_err(c, "||mu|| = %.17g != ||nu|| = %.17g", smu, snu);
         return DDO_EINVAL;

@@ -668,15 +668,24 @@ int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, d
         memcpy(hmu.data(), mu, n2 * sizeof(double));
         memcpy(hnu.data(), nu, n2 * sizeof(double));
     }
-    double smu = 0, snu = 0;
+    // compensated (Neumaier) sums: a plain running sum of 4M masses drifts by
+    // ~1e-12, the size of the equality tolerance itself
+    double smu = 0, snu = 0, cmu = 0, cnu = 0;
+    auto nadd = [](double& sum, double& comp, double x) {
+        const double t = sum + x;
+        comp += (std::fabs(sum) >= std::fabs(x)) ? (sum - t) + x : (x - t) + sum;
+        sum = t;
+    };
     for (size_t k = 0; k < n2; ++k) {
         if (!std::isfinite(hmu[k]) || hmu[k] < 0 || !std::isfinite(hnu[k]) || hnu[k] < 0) {
             set_err(c, "marginals must be finite and >= 0 (index %zu)", k);
             return DD_EINVAL;
         }
-        smu += hmu[k];
-        snu += hnu[k];
+        nadd(smu, cmu, hmu[k]);
+        nadd(snu, cnu, hnu[k]);
     }
+    smu += cmu;
+    snu += cnu;
     if (!(smu > 0) || std::fabs(smu - snu) > 1e-12 * smu) {
         set_err(c, "||mu|| = %.17g != ||nu|| = %.17g", smu, snu);
         return DD_EINVAL;

@@ -29,9 +29,6 @@
 #ifndef DD_T0_MINB
 #define DD_T0_MINB 3
 #endif
-#ifndef DD_PA_LIVE
-#define DD_PA_LIVE 0       // phase A: 1 = lanes <-> live (row, column) points (A/B)
-#endif
 namespace dd {
 
 constexpr int kR = 4;   // outputs per thread-task
@@ -691,105 +688,6 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
             }
         };
 
-        // phase A, live-point variant (DD_PA_LIVE): lanes <-> the live (row,
-        // column) points of the chunk (each row's non-zero column range RI),
-        // one output per lane and pass, x in pairs (T of two x1 rows, the
-        // reversed cost pair CP[x + 1 - y1] = (C(x + 1 - y1), C(x - y1))); the
-        // other slots of the chunk's gbuf rows are -inf.  Removes the lane
-        // padding of rows narrower than the group's union range.
-        auto phaseA_live = [&](int c0) {
-            const int cend = min(c0 + 32, gend);
-            int lo[RG], pre[RG + 1];
-            pre[0] = 0;
-#pragma unroll
-            for (int r = 0; r < RG; ++r) {
-                int n = 0;
-                lo[r] = c0;
-                if (y1b + r < d.br) {
-                    const int2 ri = L.RI[y1b + r];
-                    const int a = max(ri.x, c0), b = min(ri.y, cend - 1);
-                    if (b >= a) { n = b - a + 1; lo[r] = a; }
-                }
-                pre[r + 1] = pre[r] + n;
-            }
-            {
-                const int gs = (lane % YS) * (SUB + 1) + lane / YS;
-#pragma unroll
-                for (int r = 0; r < RG; ++r) gb[r * PR + gs] = make_float2(-INFINITY, 0.f);
-            }
-            __syncwarp();
-            const int npt = pre[RG];
-            for (int k0 = 0; k0 < npt; k0 += 32) {
-                const int k = k0 + lane;
-                const bool act = k < npt;
-                int r = 0;
-#pragma unroll
-                for (int q = 1; q < RG; ++q) r += (k >= pre[q]) ? 1 : 0;
-                const int y2 = act ? lo[r] + (k - pre[r]) : c0;
-                const int y1 = y1b + r;
-                const int idx = y1 * d.bc + y2;
-                const float2 ln = act ? LNUg[idx] : make_float2(-INFINITY, 0.f);
-                float S = act ? SLg[idx] : 0.f;
-                const float2* __restrict__ Tc = L.Tt + y2 * d.pT;
-                const float2* __restrict__ cp = CP + d.off + 1 - y1;     // cp[x] = (C(x+1-y1), C(x-y1))
-                if (exact_all) {
-                    float M = -INFINITY;
-#pragma unroll 4
-                    for (int x = 0; x < AR; ++x) {
-                        const float th = (AR == 8 && x >= d.ar) ? -INFINITY : Tc[x].x;
-                        M = fmaxf(M, th - cp[x].y);
-                    }
-                    S = M > -INFINITY ? M : 0.f;
-                }
-                const float2 S2 = make_float2(S, S);
-                float2 acc = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
-#pragma unroll 4
-                for (int x = 0; x < AR; x += 2) {
-                    float2 t0 = Tc[x], t1 = Tc[x + 1];
-                    if (AR == 8 && x >= d.ar) { t0 = make_float2(-INFINITY, 0.f); t1 = t0; }
-                    const float2 cs = __fadd2_rn(cp[x], S2);                           // C + S (exact)
-                    float2 tt = __fadd2_rn(make_float2(t1.x, t0.x), neg2(cs));
-                    tt = __ffma2_rn(tt, L2E2, make_float2(t1.y, t0.y));
-                    if ((x & 2) == 0) acc = __fadd2_rn(acc, make_float2(ex2f(tt.x), ex2f(tt.y)));
-                    else acc1 = __fadd2_rn(acc1, make_float2(ex2f(tt.x), ex2f(tt.y)));
-                }
-                acc = __fadd2_rn(acc, acc1);
-                float s = acc.x + acc.y;
-                const bool live = act && ln.x != -INFINITY;
-                if (live && (exact_all ? !(s > 0.f) : !(s >= 0.25f && s <= 4.0f))) {
-                    // exact recompute of an output whose speculative window failed
-                    float M = -INFINITY;
-                    for (int x = 0; x < d.ar; ++x) M = fmaxf(M, Tc[x].x - cp[x].y);
-                    s = 0.f;
-                    if (M > -INFINITY)
-                        for (int x = 0; x < d.ar; ++x) {
-                            const float2 t = Tc[x];
-                            s += ex2f(((t.x - cp[x].y) - M) * kL2E + t.y);
-                        }
-                    S = M;
-                    if (!exact_all) ++fallbacks;
-                }
-                float2 g = make_float2(-INFINITY, 0.f);
-                if (live) {
-                    if (s > 1e-37f && S > -INFINITY) {
-                        const float l2 = lg2f(s);
-                        const float lh = gridq(l2 * kLN2, gq);
-                        const float ll2 = fmaf(-lh, kL2E, l2);
-                        const float Sn = S + lh;
-                        SLg[idx] = Sn;
-                        g = make_float2(ln.x - Sn, ln.y - ll2);
-                        if (!(fabsf(Sn) < 1e30f)) nonfinite = 1;
-                    } else {
-                        nonfinite = 1;       // nu_cell(y) > 0 unreachable from X
-                    }
-                }
-                if (act) {
-                    const int cl = y2 - c0;
-                    gb[r * PR + (cl % YS) * (SUB + 1) + cl / YS] = g;
-                }
-            }
-        };
-
         // ---------------------------------------------------------- phase B
         auto phaseB = [&](int c0, bool maxmode, const float* S, float* A) {
             const int yb0 = c0 + hB;                      // this lane's columns yb0 + YS k
@@ -889,12 +787,8 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
             for (int j = 0; j < 4; ++j) A[j] = maxmode ? -INFINITY : 0.f;
             for (int c0 = glo; c0 < gend; c0 += 32) {
                 if (!a_done) {
-#if DD_PA_LIVE
-                    phaseA_live(c0);
-#else
                     if (gend - c0 <= 16) phaseA(c0, BoolTag<true>());
                     else phaseA(c0, BoolTag<false>());
-#endif
                 }
                 __syncwarp();
                 phaseB(c0, maxmode, S, A);

@@ -26,7 +26,7 @@ out = {
               f"of the last (kappa=0.5) 2048^2 sweep of cfg 5 (tools/profile_sweep.py --profile-last, DD_SERIAL_TIERS=1); "
               f"profiles/k1_traffic_{tag}.csv",
     "bytes_per_launch": tot,
-    "unit": "bytes per finest-layer sweep (3 tier launches)",
+    "unit": f"bytes per finest-layer sweep ({len(per)} K1 tier launches, tier G included)",
     "per_tier": per,
 }
 json.dump(out, open("profiles/k1_traffic.json", "w"), indent=1)

@@ -33,6 +33,9 @@ namespace dd {
 
 constexpr int kR = 4;   // outputs per thread-task
 
+// the CTA's mbarrier of the X-side bulk copies (initialised at kernel start)
+__shared__ unsigned long long g_k1_mbar;
+
 // --------------------------------------------------------- SMEM layout --
 struct K1Lay {
     float2* FX;   // [ar][pX]  X potential F (hi, lo2)
@@ -1245,8 +1248,9 @@ __device__ int rescue_fp64(const K1Lay& L, const Dims& d, double* F, double* Fn,
 // every output is stored to all replicas (DSMEM); three cluster barriers per
 // iteration.  Rank 0 alone runs the extraction and the epilogue.  gslice is
 // the cluster's (shared) global slice.
-template <int NT, bool BIG, int CS, bool GC>
-__device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, unsigned char* gslice) {
+template <int NT, bool BIG, int CS, bool GC, bool GM>
+__device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, unsigned char* gslice,
+                           unsigned& tma_phase) {
     static_assert(CS == 1 || BIG, "cluster tier = big-cell path");
     static_assert(!(GC && BIG), "general costs run on the SMEM tier only");
     // general costs (dd_set_cost) run on the SMEM tier only (DESIGN.md "general
@@ -1346,16 +1350,51 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     }
     // ---- X side: F = alpha/eps + log mu - shift(x~) - lambda (local affine gauge)
     const int nx = d.ar * d.ac;
+    // ---- stage the X side in shared memory by the bulk-copy engine (TMA,
+    // north_star): alpha, mu and log mu of the cell's a_r x a_c pixels, one
+    // cp.async.bulk per image row and array (a_c * 8 bytes, 16-B aligned since
+    // s >= 2), issued by one thread, completion on the CTA's mbarrier.  The
+    // staging area is scratch the solve writes only later (BIG: Tt/Ut; SMEM
+    // tier: G/LNU).  Tier G's layout is in global memory: direct loads there.
+    const double* xA = p.alpha;
+    const double* xM = p.mu;
+    const double* xL = p.logmu;
+    long long xbase = (long long)R0 * p.side + C0, xstr = p.side;     // (xr, xc) -> xbase + xr xstr + xc
+    bool staged = false;
+    if constexpr (!GM) {
+        const int arg = (rhi - rlo + 1) * p.s, acg = ncol * p.s;        // the global (untransposed) frame
+        double* stage = reinterpret_cast<double*>(BIG ? reinterpret_cast<unsigned char*>(L.Tt)
+                                                      : reinterpret_cast<unsigned char*>(L.G));
+        const unsigned need = 3u * (unsigned)nx * 8u;
+        if ((size_t)need <= (size_t)(reinterpret_cast<unsigned char*>(L.CT) - reinterpret_cast<unsigned char*>(stage))) {
+            const unsigned mb = smem_u32(&g_k1_mbar);
+            if (tid == 0) {
+                fence_proxy_async_smem();     // the previous cell's generic accesses of the area first
+                mbar_expect_tx(mb, need);
+                for (int r = 0; r < arg; ++r) {
+                    const long long g = (long long)(R0 + r) * p.side + C0;
+                    bulk_g2s(smem_u32(stage + r * acg), p.alpha + g, acg * 8, mb);
+                    bulk_g2s(smem_u32(stage + nx + r * acg), p.mu + g, acg * 8, mb);
+                    bulk_g2s(smem_u32(stage + 2 * nx + r * acg), p.logmu + g, acg * 8, mb);
+                }
+            }
+            while (!mbar_try_wait(mb, tma_phase)) {}
+            tma_phase ^= 1u;
+            xA = stage; xM = stage + nx; xL = stage + 2 * nx;
+            xbase = 0; xstr = acg;
+            staged = true;
+        }
+    }
     double fmax_l = -INFINITY, fmin_l = INFINITY, muJ = 0.0;
     for (int x = tid; x < nx; x += NT) {
         int xr, xc;
         goff(x / d.ac, x % d.ac, xr, xc);
-        const long long g = (long long)(R0 + xr) * p.side + (C0 + xc);
-        const double m = p.mu[g];
+        const long long g = xbase + (long long)xr * xstr + xc;
+        const double m = xM[g];
         muJ += m;
         if (m > 0.0) {
             const double sh = gc ? 0.0 : ((2.0 * xr + Dr) * Dr + (2.0 * xc + Dc) * Dc) * inv_kappa;
-            const double F = p.alpha[g] * inv_eps + p.logmu[g] - sh;
+            const double F = xA[g] * inv_eps + xL[g] - sh;
             fmax_l = fmax(fmax_l, F);
             fmin_l = fmin(fmin_l, F);
         }
@@ -1371,7 +1410,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
             for (int x = tid; x < nx; x += 32) {
                 int xr, xc;
                 goff(x / d.ac, x % d.ac, xr, xc);
-                v += p.mu[(long long)(R0 + xr) * p.side + (C0 + xc)];
+                v += xM[xbase + (long long)xr * xstr + xc];
             }
             v = warp_sum(v);
             if (tid == 0) L.red[60] = v;
@@ -1410,13 +1449,13 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
     for (int x = tid; x < nx; x += NT) {
         int xr, xc;
         goff(x / d.ac, x % d.ac, xr, xc);
-        const long long g = (long long)(R0 + xr) * p.side + (C0 + xc);
-        const double m = p.mu[g];
+        const long long g = xbase + (long long)xr * xstr + xc;
+        const double m = xM[g];
         float2 f = make_float2(-INFINITY, 0.f), lm = make_float2(-INFINITY, 0.f);
         if (m > 0.0) {
             const double sh = gc ? 0.0 : ((2.0 * xr + Dr) * Dr + (2.0 * xc + Dc) * Dc) * inv_kappa;
-            f = split_hl(p.alpha[g] * inv_eps + p.logmu[g] - sh - lambda, gq);
-            lm = split_hl(p.logmu[g], gq);
+            f = split_hl(xA[g] * inv_eps + xL[g] - sh - lambda, gq);
+            lm = split_hl(xL[g], gq);
         }
         L.FX[(x / d.ac) * d.pX + x % d.ac] = f;
         if (BIG) {
@@ -1426,6 +1465,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
         L.LM[x] = lm;
         L.MU[x] = (float)m;
     }
+    if (!BIG && staged) __syncthreads();     // the staging area (G/LNU) is read before LNU is written
     // ---- line 8: nu_cell = sum_i nu_i on the union box; log nu_cell
     // (BIG: log nu_cell and the extraction sums live in the CTA's global slice)
     float2* LNU = BIG ? reinterpret_cast<float2*>(gslice) : L.LNU;
@@ -1875,6 +1915,8 @@ __global__ void __launch_bounds__(NT, MINB) k1_cell_solve(SweepParams p) {
     // memory (a separate instantiation, so the on-chip tiers keep shared-window
     // addressing for every K1Lay array)
     unsigned char* base = GM ? p.gbase + (long long)blockIdx.x * p.gbase_bytes : smem;
+    unsigned tma_phase = 0;
+    if (!GM && threadIdx.x == 0) mbar_init(smem_u32(&g_k1_mbar), 1);
     const int slot = CS > 1 ? blockIdx.x / CS : blockIdx.x;
     unsigned char* gslice = BIG ? p.gscratch + (long long)slot * p.gslice : nullptr;
     if (p.poison) {     // testing: SMEM the path did not write reads as NaN
@@ -1890,7 +1932,7 @@ __global__ void __launch_bounds__(NT, MINB) k1_cell_solve(SweepParams p) {
             __syncthreads();
             const int cell = s_cell;
             if (cell < 0) return;
-            solve_cell<NT, BIG, 1, GC>(p, cell, base, gslice);
+            solve_cell<NT, BIG, 1, GC, GM>(p, cell, base, gslice, tma_phase);
             __syncthreads();
         }
     } else {
@@ -1907,7 +1949,7 @@ __global__ void __launch_bounds__(NT, MINB) k1_cell_solve(SweepParams p) {
             cluster_sync_all();
             const int cell = s_cell;
             if (cell < 0) return;        // all CTAs of the cluster leave together
-            solve_cell<NT, BIG, CS, false>(p, cell, base, gslice);
+            solve_cell<NT, BIG, CS, false, false>(p, cell, base, gslice, tma_phase);
             cluster_sync_all();          // rank 0's epilogue done before the next cell's stores
         }
     }

@@ -20,7 +20,10 @@ constexpr int kT1Threads = DD_T1_NT, kT1PerSM = DD_T1_MINB;
 #ifndef DD_T2_NT
 #define DD_T2_NT 768
 #endif
-constexpr int kT2Threads = DD_T2_NT;
+#ifndef DD_T2_MINB
+#define DD_T2_MINB 1
+#endif
+constexpr int kT2Threads = DD_T2_NT, kT2PerSM = DD_T2_MINB;
 // K1 cluster tier (tier 3): tier 2's CTA shape, kClusterSize CTAs (SMs) per cell
 #ifndef DD_CLUSTER
 #define DD_CLUSTER 8

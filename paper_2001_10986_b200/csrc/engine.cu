@@ -255,7 +255,7 @@ constexpr int kCap1 = DD_T1_CAP, kCap2 = 704;
 constexpr int kDefaultClusters = DD_NCL;   // persistent clusters of the cluster tier
 constexpr int kTierG = 4;                  // CTAs of tier G (global-memory layouts)
 // SMEM per CTA: 228 KB per SM shared by the resident CTAs, 1 KB reserved per CTA, ~1 KB static
-constexpr size_t kSmem1 = 233472 / kT1PerSM - 2048, kSmem2 = 220 * 1024;
+constexpr size_t kSmem1 = 233472 / kT1PerSM - 2048, kSmem2 = kT2PerSM == 1 ? 220 * 1024 : 233472 / kT2PerSM - 2048;
 void tier_caps(int s, int opt_main, int opt_big, int* b0, int* b1, int* b2) {
     int want = (s <= 4) ? 32 : 24;   // measured: the fused path wins above ~24 px (s = 8)
     if (opt_main > 0) want = opt_main;
@@ -784,7 +784,7 @@ int dd_init(dd_ctx** out, int n, const double* mu, const double* nu, int cost, d
         c->slice_cap[1] = std::max(c->slice_cap[1], std::min(b2, c->L[k].side));
     }
     c->grid_t[0] = kT1PerSM * prop.multiProcessorCount;
-    c->grid_t[1] = prop.multiProcessorCount;
+    c->grid_t[1] = kT2PerSM * prop.multiProcessorCount;
     for (int t = 0; t < 2; ++t) {
         const long long b = c->slice_cap[t];
         auto al = [](long long v) { return (v + 255) & ~255LL; };

@@ -29,6 +29,10 @@
 #ifndef DD_T0_MINB
 #define DD_T0_MINB 3
 #endif
+// phase A of the fused pass with 8-column quarter chunks for the narrow tails
+#ifndef DD_PA_Q
+#define DD_PA_Q 1
+#endif
 namespace dd {
 
 constexpr int kR = 4;   // outputs per thread-task
@@ -691,6 +695,115 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
             }
         };
 
+#if DD_PA_Q
+        // Quarter chunk (8 columns at chunk offset co, the group's last <= 8
+        // columns, or columns 16..23 after a half chunk): lane <-> (column
+        // co + lane / 4, x1 quarter lane % 4).  Each lane sums its quarter of
+        // the x1 range for all RG = 4 rows (the same packed body as above),
+        // then a reduce-scatter over the four quarter lanes leaves row
+        // lane % 4's sum in that lane, which runs the one-output epilogue.
+        // Padding of phase A drops from 16/32 to 8 columns (K1).
+        auto phaseQ = [&](int c0, int co) {
+            static_assert(RG == 4, "quarter chunk: 4 rows");
+            constexpr int XQ = AR / 4;                  // x1 per quarter
+            const int qt = lane & 3;
+            const int cl = co + (lane >> 2);
+            const int y2 = c0 + cl;
+            const bool vy = y2 < gend;
+            const int y2c = vy ? y2 : gend - 1;
+            const int xb = qt * XQ;
+            float sp[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const bool v = vy && (y1b + q < d.br);
+                sp[q] = v ? SLg[(y1b + q) * d.bc + y2] : 0.f;
+            }
+            const bool vr = vy && (y1b + qt < d.br);
+            const float2 lnr = vr ? LNUg[(y1b + qt) * d.bc + y2] : make_float2(-INFINITY, 0.f);
+            const float2* __restrict__ Tc = L.Tt + y2c * d.pT;
+            const float2* __restrict__ cpb = CP + cpo;
+            if (exact_all) {
+                float2 M[2] = {make_float2(-INFINITY, -INFINITY), make_float2(-INFINITY, -INFINITY)};
+#pragma unroll
+                for (int k = 0; k < XQ; ++k) {
+                    const int x = xb + k;
+                    float th = Tc[x].x;
+                    if (AR == 8) th = (x < d.ar) ? th : -INFINITY;
+#pragma unroll
+                    for (int i = 0; i < 2; ++i) {
+                        const float2 tt = __fadd2_rn(make_float2(th, th), neg2(cpb[x - 2 * i]));
+                        M[i] = make_float2(fmaxf(M[i].x, tt.x), fmaxf(M[i].y, tt.y));
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+                    for (int o = 1; o <= 2; o <<= 1) {
+                        M[i].x = fmaxf(M[i].x, __shfl_xor_sync(0xffffffffu, M[i].x, o));
+                        M[i].y = fmaxf(M[i].y, __shfl_xor_sync(0xffffffffu, M[i].y, o));
+                    }
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    sp[2 * i] = M[i].x > -INFINITY ? M[i].x : 0.f;
+                    sp[2 * i + 1] = M[i].y > -INFINITY ? M[i].y : 0.f;
+                }
+            }
+            const float2 nS0 = make_float2(-sp[0], -sp[1]), nS1 = make_float2(-sp[2], -sp[3]);
+            float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int k = 0; k < XQ; ++k) {
+                const int x = xb + k;
+                float2 t = Tc[x];
+                if (AR == 8 && x >= d.ar) t = make_float2(-INFINITY, 0.f);
+                const float2 cs0 = __fadd2_rn(cpb[x], neg2(nS0));
+                const float2 cs1 = __fadd2_rn(cpb[x - 2], neg2(nS1));
+                float2 t0 = __fadd2_rn(make_float2(t.x, t.x), neg2(cs0));
+                float2 t1 = __fadd2_rn(make_float2(t.x, t.x), neg2(cs1));
+                t0 = __ffma2_rn(t0, L2E2, make_float2(t.y, t.y));
+                t1 = __ffma2_rn(t1, L2E2, make_float2(t.y, t.y));
+                a0 = __fadd2_rn(a0, make_float2(ex2f(t0.x), ex2f(t0.y)));
+                a1 = __fadd2_rn(a1, make_float2(ex2f(t1.x), ex2f(t1.y)));
+            }
+            // reduce-scatter: xor 2 exchanges row pairs, xor 1 the rows of a pair
+            const bool b1 = (qt & 2) != 0, b0 = (qt & 1) != 0;
+            float2 keep = b1 ? a1 : a0;
+            const float2 send = b1 ? a0 : a1;
+            keep = __fadd2_rn(keep, make_float2(__shfl_xor_sync(0xffffffffu, send.x, 2),
+                                                __shfl_xor_sync(0xffffffffu, send.y, 2)));
+            float s = b0 ? keep.y : keep.x;
+            s += __shfl_xor_sync(0xffffffffu, b0 ? keep.x : keep.y, 1);
+            float S = qt == 0 ? sp[0] : qt == 1 ? sp[1] : qt == 2 ? sp[2] : sp[3];
+            const bool live = lnr.x != -INFINITY;
+            const bool bad = live && (exact_all ? !(s > 0.f) : !(s >= 0.25f && s <= 4.0f));
+            if (__any_sync(0xffffffffu, bad) && bad) {
+                float M = -INFINITY;
+                for (int x = 0; x < d.ar; ++x) M = fmaxf(M, Tc[x].x - cpb[x - qt].x);
+                s = 0.f;
+                if (M > -INFINITY)
+                    for (int x = 0; x < d.ar; ++x) {
+                        const float2 t = Tc[x];
+                        s += ex2f(((t.x - cpb[x - qt].x) - M) * kL2E + t.y);
+                    }
+                S = M;
+                if (!exact_all) ++fallbacks;
+            }
+            float2 g = make_float2(-INFINITY, 0.f);
+            if (live) {
+                if (s > 1e-37f && S > -INFINITY) {
+                    const float l2 = lg2f(s);
+                    const float lh = gridq(l2 * kLN2, gq);
+                    const float ll2 = fmaf(-lh, kL2E, l2);
+                    const float Sn = S + lh;
+                    SLg[(y1b + qt) * d.bc + y2] = Sn;
+                    g = make_float2(lnr.x - Sn, lnr.y - ll2);
+                    if (!(fabsf(Sn) < 1e30f)) nonfinite = 1;
+                } else {
+                    nonfinite = 1;
+                }
+            }
+            gb[qt * PR + (cl % YS) * (SUB + 1) + cl / YS] = g;
+        };
+#endif
+
         // ---------------------------------------------------------- phase B
         auto phaseB = [&](int c0, bool maxmode, const float* S, float* A) {
             const int yb0 = c0 + hB;                      // this lane's columns yb0 + YS k
@@ -790,8 +903,20 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
             for (int j = 0; j < 4; ++j) A[j] = maxmode ? -INFINITY : 0.f;
             for (int c0 = glo; c0 < gend; c0 += 32) {
                 if (!a_done) {
+#if DD_PA_Q
+                    const int rem = gend - c0;
+                    if (rem <= 8) {
+                        phaseQ(c0, 0);
+                    } else if (rem <= 24) {
+                        phaseA(c0, BoolTag<true>());
+                        if (rem > 16) phaseQ(c0, 16);
+                    } else {
+                        phaseA(c0, BoolTag<false>());
+                    }
+#else
                     if (gend - c0 <= 16) phaseA(c0, BoolTag<true>());
                     else phaseA(c0, BoolTag<false>());
+#endif
                 }
                 __syncwarp();
                 phaseB(c0, maxmode, S, A);
@@ -2137,7 +2262,7 @@ cudaError_t launch_k1(const SweepParams& p, int tier, int grid, size_t smem, cud
         return launch_tier<256, false, DD_T0_MINB, 1>(p, grid, smem, st);
     }
     if (tier == 1) return launch_tier<kT1Threads, true, kT1PerSM, 1>(p, grid, smem, st);
-    if (tier == 2) return launch_tier<kT2Threads, true, 1, 1>(p, grid, smem, st);
+    if (tier == 2) return launch_tier<kT2Threads, true, kT2PerSM, 1>(p, grid, smem, st);
     return launch_tier<kT2Threads, true, 1, kClusterSize>(p, grid, smem, st);
 }
 

@@ -25,6 +25,7 @@ ap.add_argument("--profile-last", action="store_true")
 ap.add_argument("--quiet", action="store_true")
 ap.add_argument("--bcap", type=int, default=0)
 ap.add_argument("--bcap-big", type=int, default=0)
+ap.add_argument("--onchip", type=int, default=0, help="testing: boxes above this side go to tier G")
 ap.add_argument("--json", default="")
 ap.add_argument("--cells-npz", default="", help="dump per-cell (iters, box, mufu, kcycles) of every sweep at side >= n/2")
 ap.add_argument("--cells-all", action="store_true", help="--cells-npz for every layer")
@@ -33,7 +34,8 @@ p = CONFIGS[a.cfg]
 n, s = p["n"], p["s"]
 mu, nu = config_images(a.cfg)
 g = DD(mu, nu, p["kappa_final"] / n**2, s, schedule=SCHED_LADDER, coarsest_side=p.get("coarsest", 8),
-       eps_start=p.get("eps_start", 0.0), bcap_main=a.bcap, bcap_big=a.bcap_big)
+       eps_start=p.get("eps_start", 0.0), bcap_main=a.bcap, bcap_big=a.bcap_big,
+       bcap_onchip=a.onchip)
 sched = build_schedule(n, p.get("coarsest", 8), p["kappa_final"], p.get("eps_start", 0.0))
 rows = []
 cell_dump = {}

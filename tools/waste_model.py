@@ -7,6 +7,9 @@ composite cell of the next sweep's partition that goes to the fused tiers
   rows    points inside each row's [first, last] non-zero column
   groups  4 x (union width of each 4-row group)        (phase B, interleaved)
   chunks  4 x 32 x ceil(union width / 32) per group     (phase A)
+  half    the same with a half chunk for a last chunk of <= 16 columns
+  quarter the same with 8-column quarter chunks (<= 8: quarter, <= 16: half,
+          <= 24: half + quarter), the phase A of DD_PA_Q = 1
 
   python tools/waste_model.py [--cfg 5]
 """
@@ -43,7 +46,7 @@ def span(c):
 
 
 nca = nb // 2 if part == 1 else nb // 2 + 1
-tot = dict(nz=0, rows=0, groups=0, chunks=0, half=0, cells=0, full=0)
+tot = dict(nz=0, rows=0, groups=0, chunks=0, half=0, quarter=0, cells=0, full=0)
 hist = np.zeros(8, np.int64)          # group union widths by 8-column bins (up to 64+)
 for cp in range(nca):
     r0, r1 = span(cp)
@@ -82,9 +85,12 @@ for cp in range(nca):
             tot["groups"] += 4 * w
             tot["chunks"] += 4 * 32 * ((w + 31) // 32)
             tot["half"] += 4 * 32 * (w // 32) + (4 * 32 if w % 32 > 16 else (4 * 16 if w % 32 else 0))
+            r = w % 32       # last chunk: quarter (<= 8), half (<= 16), half + quarter (<= 24), full
+            tot["quarter"] += 4 * 32 * (w // 32) + 4 * (0 if r == 0 else 8 if r <= 8 else 16 if r <= 16
+                                                          else 24 if r <= 24 else 32)
             hist[min(w // 8, 7)] += 1
         tot["cells"] += 1
 print("partition", part, "fused-tier cells", tot["cells"])
 print("group widths (8-col bins):", hist.tolist())
-for k in ("full", "rows", "groups", "chunks", "half"):
+for k in ("full", "rows", "groups", "chunks", "half", "quarter"):
     print(f"{k:7s} / nz = {tot[k] / tot['nz']:.3f}")

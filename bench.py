@@ -47,6 +47,10 @@ def _args():
                     help="1: a step solves the image pairs concurrently (dd_run_schedule_batch); "
                          "0: a step is one pair (they cycle)")
     ap.add_argument("--max-inner-iter", type=int, default=100000)
+    ap.add_argument("--allow-flagged", type=int, default=-1, choices=[-1, 0, 1],
+                    help="1: cells flagged at max_inner_iter / by a failed fp64 rescue (reading A6; they keep "
+                         "their Y-feasible plan) do not abort the run, their count is reported as totals.failed; "
+                         "default: on for --config 4 (4 such border cells of ~1e-6 mass), off for the headline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -160,6 +164,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     w = _workload(args.config)
+    strict = not (args.allow_flagged == 1 or (args.allow_flagged == -1 and args.config == 4))
     samples = []
     for _ in range(args.warmup if args.warmup < 1 else 0):
         pass
@@ -325,6 +330,7 @@ def main():
     from paper_2001_10986_b200 import DD, SCHED_LADDER, measure_mufu_peak
     from paper_2001_10986_b200.dd import run_schedule_batch
     w = _workload(args.config)
+    strict = not (args.allow_flagged == 1 or (args.allow_flagged == -1 and args.config == 4))
     n, s = w["n"], w["s"]
     eps = w["kappa_final"] / n**2
     stream = torch.cuda.Stream(dev)          # a real stream handle (the default stream is 0)
@@ -361,7 +367,7 @@ def main():
     def solve(ctx, striped):
         """One full coarse-to-fine solve (the bench step)."""
         if striped is None:
-            ctx.run_schedule()
+            ctx.run_schedule(check=strict)
         else:
             striped.run_schedule(n, w["coarsest"], w["kappa_final"], w["eps_start"])
 
@@ -369,18 +375,18 @@ def main():
         for c in cs:
             c.reset()
         for c in cs:
-            c.synchronize()
+            c.synchronize(check=strict)
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     for k in range(args.warmup if batched else max(args.warmup, npairs if args.warmup > 0 else 0)):
         if batched:
             reset_all(ctxs)
-            run_schedule_batch(ctxs)
+            run_schedule_batch(ctxs, check=strict)
         else:
             c = ctxs[k % npairs]
             c.reset()
             solve(c, run)
-            c.synchronize()
+            c.synchronize(check=strict)
     # ---- timed region: K steps (pair k mod 5), per-step CUDA events on the library's stream
     for c in ctxs:
         c.reset_totals()
@@ -398,7 +404,7 @@ def main():
             reset_all(ctxs)                    # states back to the product coupling (untimed)
             torch.cuda.synchronize(dev)
             e0.record(stream)                  # ctxs[0]'s stream orders the batch (dd.h)
-            run_schedule_batch(ctxs)
+            run_schedule_batch(ctxs, check=strict)
             e1.record(stream)
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
@@ -439,12 +445,12 @@ def main():
         lat = {}
         for k, c in enumerate(ctxs):
             c.reset()
-            c.synchronize()
+            c.synchronize(check=strict)
             torch.cuda.synchronize(dev)
             a0 = torch.cuda.Event(enable_timing=True)
             a1 = torch.cuda.Event(enable_timing=True)
             a0.record(streams[k])
-            c.run_schedule()
+            c.run_schedule(check=strict)
             a1.record(streams[k])
             a1.synchronize()
             lat[str(k)] = a0.elapsed_time(a1)
@@ -471,7 +477,7 @@ def main():
         l1x, l1y = run.marginal_error()
         gap = None
     else:
-        g.synchronize()
+        g.synchronize(check=strict)
         cost, ent = g.primal_cost()
         l1x, l1y = g.marginal_error()
         t0 = time.perf_counter()
@@ -520,7 +526,7 @@ def main():
             t0 = time.perf_counter()
             ges = [DD(a.numpy(), b.numpy(), eps, s, stream=streams[i].cuda_stream, **kw)
                    for i, (a, b) in enumerate(pinned)]
-            run_schedule_batch(ges)
+            run_schedule_batch(ges, check=strict)
             res = [(ge.primal_cost(), ge.marginal_error()) for ge in ges]
             dt = time.perf_counter() - t0
             for ge in ges:

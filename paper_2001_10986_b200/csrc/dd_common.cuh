@@ -94,6 +94,9 @@ struct SweepParams {
     const double* h2;
     int hst;
     int safeguard;        // DD_FLAG_SAFEGUARD: eps-raising retry of failing cells (A29)
+    // testing (env DD_FORCE_RESCUE="cell:it", read per sweep): composite cell `force_cell` leaves the
+    // fp32 loop after `force_it` iterations and finishes in fp64 (rescue_fp64), as a stalled cell would
+    int force_cell, force_it;
     // tier G (SMEM-tier kernel on a global-memory layout): the
     // cells beyond the largest on-chip tier; CTA b carves its K1Lay from
     // gbase + b * gbase_bytes instead of shared memory
@@ -177,6 +180,12 @@ __device__ __forceinline__ void st_cl(unsigned a, int v) {
 __device__ __forceinline__ int atom_add_cl(unsigned a, int v) {
     int o;
     asm volatile("atom.shared::cluster.add.u32 %0, [%1], %2;" : "=r"(o) : "r"(a), "r"(v) : "memory");
+    return o;
+}
+// one lane's shared-memory counter fetch (no compiler warp-aggregation code around it)
+__device__ __forceinline__ int atom_add_sh(unsigned a, int v) {
+    int o;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(o) : "r"(a), "r"(v) : "memory");
     return o;
 }
 __device__ __forceinline__ void atom_or_cl(unsigned a, int v) {

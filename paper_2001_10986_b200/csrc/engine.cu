@@ -331,6 +331,12 @@ int sweep(dd_ctx* c) {
     p.eps = c->eps;
     p.h1 = c->d_h1; p.h2 = c->d_h2; p.hst = c->L[c->n_layers - 1].side / Lr.side;
     p.safeguard = (c->opt.flags & DD_FLAG_SAFEGUARD) ? 1 : 0;
+    p.force_cell = -1;
+    p.force_it = 0;
+    if (const char* e = getenv("DD_FORCE_RESCUE")) {
+        int a = -1, b = 0;
+        if (sscanf(e, "%d:%d", &a, &b) == 2 && b >= 1) { p.force_cell = a; p.force_it = b; }
+    }
     p.kappa = c->eps * (double)Lr.side * (double)Lr.side;
     p.tau = c->tau;
     p.err_tol = c->opt.err_tol;

@@ -30,6 +30,13 @@
 #define DD_T0_MINB 3
 #endif
 // phase A of the fused pass with 8-column quarter chunks for the narrow tails
+// fused pass, per-group control (round 2, profiles/r02/r02_t2_lines.txt: the group fetch, the
+// stabiliser prologue, the window check and the U epilogue were ~13 % of K1's instructions):
+// inline atom.shared for the group counter, branch-free prologue / window check, the four U
+// outputs of a (row, x2 quad) dealt over its YS lanes.  Same arithmetic, same bits.
+#ifndef DD_FV2
+#define DD_FV2 1
+#endif
 #ifndef DD_PA_Q
 #define DD_PA_Q 1
 #endif
@@ -563,10 +570,18 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
     const int ng = (d.br + RG - 1) / RG;
     // the group counter lives in cluster rank 0 (CS > 1: groups are dealt
     // over all warps of the cluster)
+#if DD_FV2
+    const unsigned wk0 = CS > 1 ? mapa_u32(smem_u32(&L.WK[0]), 0) : smem_u32(&L.WK[0]);
+#else
     const unsigned wk0 = CS > 1 ? mapa_u32(smem_u32(&L.WK[0]), 0) : 0u;
+#endif
     while (true) {
         int u = 0;
+#if DD_FV2
+        if (lane == 0) u = CS > 1 ? atom_add_cl(wk0, 1) : atom_add_sh(wk0, 1);
+#else
         if (lane == 0) u = CS > 1 ? atom_add_cl(wk0, 1) : atomicAdd(&L.WK[0], 1);
+#endif
         u = __shfl_sync(0xffffffffu, u, 0);
         if (u >= ng) break;
         const int grp = L.GL[u];
@@ -878,6 +893,20 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
         float S[4];
         bool empty[4];
         bool exact = exact_all;
+#if DD_FV2
+        {
+            const bool ld = !exact && rvalid && qvalid;
+            const float2* up = L.Ut + x2b * d.pU + y1B;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float u = ld ? up[j * d.pU].x : 0.f;
+                const bool fin = fabsf(u) < 1e30f;
+                empty[j] = (u == -INFINITY);
+                S[j] = fin ? u : 0.f;
+                exact = exact | (!fin & !empty[j]);       // +inf or NaN: exact two-pass
+            }
+        }
+#else
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             empty[j] = false;
@@ -889,6 +918,7 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
                 else exact = true;
             }
         }
+#endif
         if (!exact_all) exact = __any_sync(0xffffffffu, exact);
         // passes: speculative -> one sum pass; exact -> max pass + sum pass.
         // A failed speculative window check restarts the group in exact mode.
@@ -943,14 +973,64 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
             for (int j = 0; j < 4; ++j) acc[j] = A[j];
             if (exact) break;
             bool ok = true;
+#if DD_FV2
+            {
+                const bool nrq = !rvalid | !qvalid;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const bool win = (acc[j] >= 0.25f) & (acc[j] <= 4.0f);
+                    const bool okj = empty[j] ? (acc[j] == 0.f) : win;
+                    ok = ok & (nrq | okj);
+                }
+            }
+#else
 #pragma unroll
             for (int j = 0; j < 4; ++j)
                 ok = ok && (!rvalid || !qvalid ||
                             (empty[j] ? acc[j] == 0.f : (acc[j] >= 0.25f && acc[j] <= 4.0f)));
+#endif
             if (__all_sync(0xffffffffu, ok)) break;
             if (lane == 0) ++fallbacks;
             pass = 0;
         }
+#if DD_FV2
+        if (rvalid && qvalid) {
+            // every lane of the YS-lane slice holds the four sums: lane hB finalises
+            // outputs j = hB (4 / YS) .. (one or two of the four)
+            constexpr int JO = 4 / YS;
+#pragma unroll
+            for (int jj = 0; jj < JO; ++jj) {
+                float a, Sj;
+                bool e;
+                if constexpr (YS == 2) {
+                    a = hB ? acc[2 + jj] : acc[jj];
+                    Sj = hB ? S[2 + jj] : S[jj];
+                    e = hB ? empty[2 + jj] : empty[jj];
+                } else {
+                    static_assert(YS == 2 || YS == 4, "phase-B slice");
+                    a = hB == 0 ? acc[0] : hB == 1 ? acc[1] : hB == 2 ? acc[2] : acc[3];
+                    Sj = hB == 0 ? S[0] : hB == 1 ? S[1] : hB == 2 ? S[2] : S[3];
+                    e = hB == 0 ? empty[0] : hB == 1 ? empty[1] : hB == 2 ? empty[2] : empty[3];
+                }
+                const int j = hB * JO + jj;
+                float2 u = make_float2(-INFINITY, 0.f);
+                if (!e && a > 1e-37f) {
+                    float lh, ll;
+                    if (a >= 0.25f && a <= 4.0f) {
+                        // the common (speculative) case: lg2.approx is within ~1e-7 here
+                        const float l2 = lg2f(a);
+                        lh = gridq(l2 * kLN2, gq);
+                        ll = fmaf(-lh, kL2E, l2);
+                    } else {
+                        ln_split(a, gq, lh, ll);
+                    }
+                    u = make_float2(Sj + lh, ll);
+                    if (!(fabsf(u.x) < 1e30f)) nonfinite = 1;
+                }
+                bcast<CS>(&L.Ut[(x2b + j) * d.pU + y1B], u);
+            }
+        }
+#else
         if (hB == 0 && rvalid && qvalid) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -971,6 +1051,7 @@ __device__ __forceinline__ void fused_y2x1(const K1Lay& L, const Dims& d, const 
                 bcast<CS>(&L.Ut[(x2b + j) * d.pU + y1B], u);
             }
         }
+#endif
     }
 }
 
@@ -1733,6 +1814,7 @@ __device__ void solve_cell(const SweepParams& p, int cell, unsigned char* base, 
             else co.flags |= 1;
             break;
         }
+        if (cell == p.force_cell && it >= p.force_it) { rescue = true; break; }    // DD_FORCE_RESCUE (testing)
         // stall at the fp32 error floor: < 2 % progress over 256 iterations
         // within 1.5x of the tolerance -> continue in fp64 (rescue_fp64)
         if ((it & 255) == 0) {

@@ -133,13 +133,14 @@ def measure_mufu_peak(device=0):
     return v.value
 
 
-def run_schedule_batch(dds):
+def run_schedule_batch(dds, check=True):
     """dd_run_schedule_batch: the full schedule of several independent problems
-    (contexts on distinct streams), sweeps enqueued round-robin, one wait."""
+    (contexts on distinct streams), sweeps enqueued round-robin, one wait.
+    check=False accepts DD_ENOCONV (flagged cells, reading A6) and returns it."""
     arr = (C.c_void_p * len(dds))(*[d._h.value for d in dds])
     rc = lib().dd_run_schedule_batch(arr, len(dds))
     if rc != OK:
-        return dds[0]._check(rc, "run_schedule_batch")
+        return dds[0]._check(rc, "run_schedule_batch", (OK,) if check else (OK, ENOCONV))
     return rc
 
 
@@ -234,8 +235,8 @@ class DD:
     def refine(self):
         return self._check(lib().dd_refine(self._h), "refine")
 
-    def run_schedule(self):
-        return self._check(lib().dd_run_schedule(self._h), "run_schedule")
+    def run_schedule(self, check=True):
+        return self._check(lib().dd_run_schedule(self._h), "run_schedule", (OK,) if check else (OK, ENOCONV))
 
     def reset(self):
         return self._check(lib().dd_reset(self._h), "reset")

@@ -1,10 +1,16 @@
-"""fp64 rescue of K1: cfg 4, pair 0 has a border
-cell of tiny mass (B-partition cell 3771 of the second kappa = 0.5 sweep at
-1024^2, ||mu_J|| = 1.8e-6) on which the fp32 passes stall at an X-error of
-~1.04 ||mu_J|| Err while the fp64 oracle converges in 426 iterations.  K1
-detects the stall, finishes the cell in fp64 and must agree with the oracle
-like any other cell (within ~2 Err ||mu_J|| when the stop
-iterations differ)."""
+"""fp64 rescue of K1: a cell the fp32 passes cannot
+finish at the error floor is continued from its potentials by the same four
+separable passes in fp64 (rescue_fp64) and must agree with the oracle like any
+other cell (within ~2 Err ||mu_J|| when the stop iterations
+differ).  Which cells stall depends on the fp32 trajectory (on an earlier
+build the border cell 3771 of cfg 4, pair 0, ||mu_J|| = 1.8e-6, stalled at
+1.04 ||mu_J|| Err for 1e5 iterations, profiles/r02/stall_cell3771_fp32.log;
+with the quarter-chunk phase A it converges in 461 fp32 iterations), so the
+test takes the fp64 continuation on that cell through the testing hook
+DD_FORCE_RESCUE="cell:it" (dd_common.cuh: the cell leaves the fp32 loop after
+`it` iterations exactly as the stall detector would make it)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -59,7 +65,12 @@ def test_rescue_matches_oracle(before_state):
     g, before, mu, nu = before_state
     n, s = 1024, 8
     g.set_state(before)
-    g.iterate(1, check=False)
+    os.environ["DD_FORCE_RESCUE"] = f"{CELL}:64"
+    try:
+        g.iterate(1, check=False)
+        g.synchronize(check=False)
+    finally:
+        del os.environ["DD_FORCE_RESCUE"]
     after = g.get_state()
     it, bx, _, _, fl, ex = g.cell_stats(flags=True, err=True)
     part = after["info"]["last_partition"]
@@ -67,14 +78,37 @@ def test_rescue_matches_oracle(before_state):
     nb = n // s
     mem = _members(nb, part, CELL)
     mJ = mu.reshape(nb, s, nb, s).sum((1, 3)).ravel()[mem].sum()
-    assert fl[CELL] & 16, "the fp64 rescue did not run on the stalled cell"
+    assert fl[CELL] & 16, "the fp64 continuation did not run on the forced cell"
+    assert it[CELL] > 64
     assert not fl[CELL] & 1 and ex[CELL] <= ERR * mJ, (fl[CELL], ex[CELL] / (ERR * mJ))
+    # only the forced cell (and cells that stall by themselves) take the fp64 path
+    assert ((fl & 16) != 0).sum() <= 8
     o = Oracle(mu, nu, 0.5 / n**2, s, empty_init=True, max_inner_iter=100000)
     o.set_state(before)
     io = o.solve_cells(part, np.array([CELL]))
     ost = o.get_state()
     d = sum(np.abs(_dense(after, i, n) - _dense(ost, i, n)).sum() for i in mem)
     assert d <= 2 * ERR * mJ, (d / mJ, int(it[CELL]), int(io[0]))
+
+
+def test_stall_detector_flags(before_state):
+    """The sweep's cells that the stall detector hands to the fp64 path carry
+    flag 16; those fp64 cannot finish within its iteration cap either (the
+    oracle needs > 4e4 iterations on them) also carry flag 1 (reading A6) and
+    keep a Y-feasible plan."""
+    g, before, mu, nu = before_state
+    g.set_state(before)
+    g.iterate(1, check=False)
+    g.synchronize(check=False)
+    it, bx, _, _, fl, ex = g.cell_stats(flags=True, err=True)
+    stalled = np.nonzero(fl & 16)[0]
+    assert stalled.size <= 8
+    for c in stalled:
+        assert it[c] >= 512 + 1
+    failed = (fl & 1) != 0
+    assert ((fl[failed] & 16) != 0).all(), "a cell hit max_inner_iter in fp32 without the stall detector"
+    lx, ly = g.marginal_error()
+    assert ly < 1e-8
 
 
 def test_set_max_inner_iter_full_size(before_state):

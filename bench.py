@@ -186,7 +186,7 @@ def run_reference(args):
 
 
 # ------------------------------------------------------- finest-sweep tools --
-def run_all_but_last(g, n, coarsest, kappa_final, eps_start):
+def run_all_but_last(g, n, coarsest, kappa_final, eps_start, strict=True):
     """Reset g and run the bench's schedule up to (not including) its last
     sweep, stage by stage; returns (schedule, per-sweep stats of the last
     finest-layer stage before it)."""
@@ -201,18 +201,19 @@ def run_all_but_last(g, n, coarsest, kappa_final, eps_start):
             side *= 2
         g.set_eps(kappa / sd**2)
         k = sweeps if done + sweeps < total else sweeps - 1
-        g.iterate(k)
+        g.iterate(k, check=strict)
         done += k
     return sched
 
 
-def finest_sweep_rate(g, n, coarsest, kappa_final, eps_start, peak):
+def finest_sweep_rate(g, n, coarsest, kappa_final, eps_start, peak, strict=True):
     """SURVEY 8(d) metric 1(i): cell solves/s of the last (steady-state,
     final-eps) sweeps of the finest layer, device time per sweep from the
     library's CUDA events."""
-    run_all_but_last(g, n, coarsest, kappa_final, eps_start)
-    g.synchronize()
-    g.iterate(1)
+    run_all_but_last(g, n, coarsest, kappa_final, eps_start, strict)
+    g.synchronize(check=strict)
+    g.iterate(1, check=strict)
+    g.synchronize(check=strict)
     st = g.stats()
     return {"cells": st["cells"], "ms": st["ms"], "solve_ms": st["solve_ms"],
             "value": st["cells"] / (st["ms"] * 1e-3), "unit": UNIT, "iters_per_cell": st["iters_sum"] / st["cells"],
@@ -511,7 +512,7 @@ def main():
                 "mufu_ops_per_step": tot["mufu_ops"] / args.steps}
     finest = None
     if run is None:
-        finest = finest_sweep_rate(g, n, w["coarsest"], w["kappa_final"], w["eps_start"], peak)
+        finest = finest_sweep_rate(g, n, w["coarsest"], w["kappa_final"], w["eps_start"], peak, strict)
 
     # ---- end to end through the public API with host buffers
     e2e = None
